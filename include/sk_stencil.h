@@ -1,0 +1,181 @@
+/*
+ * sk_stencil.h — C-ABI of the B200 SkelCL-style 2D stencil executor.
+ *
+ * This is the drop-in boundary that replaces the reference's simulated
+ * execution seam (wgtune "simoracle", /root/reference/proj/include/wgtune/
+ * simoracle.hpp) with real sm_100a kernels.  Plain pointers and sizes only:
+ * no torch, no C++ types.  Every entry point names the reference interface it
+ * replaces.
+ *
+ * Grid semantics (Fig. 1 at :122-128): a row-major H x W
+ * matrix (row pitch >= W elements).  Each output cell is the customising
+ * function applied to the rectangular border region around the input cell:
+ * `north` rows above (row - 1 ... row - north), `south` rows below,
+ * `east` columns to the right (col + 1 ...), `west` columns to the left.
+ * Cells of the region outside the matrix take the pad value (SK_BORDER_PAD)
+ * or the value of the nearest in-matrix cell (SK_BORDER_NEAREST, i.e.
+ * clamp(row), clamp(col)).  The workgroup (CUDA block) is wc columns by wr
+ * rows of work-items, one work-item per output cell; each block stages its
+ * tile plus the perimeter border region in shared memory (PAPER.md:102-111,
+ * tile shape (wc+E+W) x (wr+N+S) as in simoracle.cpp:21-28).
+ */
+#ifndef SK_STENCIL_H
+#define SK_STENCIL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  SK_OVERSIZED / SK_REFUSED mirror the reference's
+ * ProbeResult{Legal, Refused, Oversized} (tuner.hpp:16) and the exceptions
+ * IllegalWorkgroupSize (errors.hpp:27) / RefusedParameter (errors.hpp:52-63)
+ * thrown by simoracle::run (simoracle.cpp:122-131).  A refusal is a real,
+ * non-sticky launch-configuration failure on the device (shared-memory tile
+ * above the opt-in limit, no resident block possible, launch-config error);
+ * a sticky CUDA fault is SK_ECUDA and aborts sweeps. */
+typedef enum {
+  SK_OK = 0,
+  SK_OVERSIZED = 1, /* wc*wr above min(device max, per-kernel max)        */
+  SK_REFUSED = 2,   /* legal size the device refuses to launch            */
+  SK_EINVAL = 3,    /* bad argument (null pointer, bad enum, bad dims)    */
+  SK_ECUDA = 4,     /* CUDA runtime error; see sk_last_error()            */
+  SK_ENOTSUP = 5    /* combination not supported (e.g. in/out dtype mix)  */
+} sk_status;
+
+/* Element types, in the order of the reference's ElementType
+ * (scenario.hpp:14: INT32, FLOAT32, FLOAT64). */
+typedef enum { SK_INT32 = 0, SK_FLOAT32 = 1, SK_FLOAT64 = 2 } sk_dtype;
+
+/* Border substitution. */
+typedef enum { SK_BORDER_PAD = 0, SK_BORDER_NEAREST = 1 } sk_border_mode;
+
+/* Customising functions.  The formulas are defined once in DESIGN.md §3 and
+ * restated independently by the CPU oracle (oracle/stencil_oracle.c).
+ * The real-world kernel set follows the reference's reference_kernels()
+ * (synthgen.cpp:82-96 / PAPER.md Table 2): gaussian, gol, he, nms, sobel,
+ * threshold; the synthetic family follows generate_kernels()
+ * (synthgen.cpp:57-80).  FIVE_POINT and BOXMEAN are the BASELINE.json
+ * config-1 and config-4 kernels. */
+typedef enum {
+  SK_OP_FIVE_POINT = 0, /* mean of centre + 4 neighbours, border (1,1,1,1)  */
+  SK_OP_HEAT = 1,       /* "he": u + 0.2*(n+s+e+w-4u), border (1,1,1,1)     */
+  SK_OP_GOL = 2,        /* "gol": Conway B3/S23, 3x3 Moore, border 1        */
+  SK_OP_BOXMEAN = 3,    /* mean of the whole N/S/E/W region (any borders)   */
+  SK_OP_GAUSSIAN = 4,   /* "gaussian": binomial blur, border g in [1,10]    */
+  SK_OP_SOBEL = 5,      /* "sobel": gradient magnitude, border 1            */
+  SK_OP_NMS = 6,        /* "nms": keep local 3x3 maxima, border 1           */
+  SK_OP_THRESHOLD = 7,  /* "threshold": c > 0.5 ? 1 : 0, border 0           */
+  SK_OP_SYNTHETIC = 8,  /* "synthetic-*": cross-shaped region mean + ALU loop */
+  SK_OP_COUNT = 9
+} sk_op;
+
+/* Load strategy for the shared-memory tile. */
+typedef enum {
+  SK_LOAD_AUTO = 0,     /* TMA when the tile/tensor constraints allow       */
+  SK_LOAD_TMA = 1,      /* force the TMA-pipelined persistent kernel        */
+  SK_LOAD_EXPLICIT = 2  /* force explicit coalesced loads (one tile/block)  */
+} sk_load_path;
+
+/* Stencil descriptor: the kernel half of a reference KernelDescriptor
+ * (scenario.hpp:46-56: name -> op, north/south/east/west, complexity,
+ * total_instructions) plus the element type (DatasetDescriptor in/out type,
+ * scenario.hpp:58-66; in == out) and the border mode / pad value that the
+ * SkelCL user chooses. */
+typedef struct {
+  int32_t op;          /* sk_op                                             */
+  int32_t dtype;       /* sk_dtype, input and output                        */
+  int32_t north, south, east, west; /* border region, each in [0, 64]       */
+  int32_t border_mode; /* sk_border_mode                                    */
+  double pad_value;    /* cast to the element type                          */
+  int32_t complexity;  /* synthetic only: 0 light (synthetic-a), 1 heavy (b) */
+  int32_t instructions;/* synthetic only: static instruction total          */
+  int32_t load_path;   /* sk_load_path                                      */
+} sk_stencil_desc;
+
+/* Launch one stencil pass over a W x H region, out-of-place, on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  `d_in` points at row 0 of
+ * the region; `rows_above` / `rows_below` further input rows are readable
+ * beyond it (halo rows of a row shard, §8e) and are used as real data before
+ * border substitution applies.  Replaces: simoracle::run
+ * (simoracle.hpp:45, simoracle.cpp:122-141) for one sample. */
+int sk_stencil_launch(const sk_stencil_desc* desc, const void* d_in, void* d_out,
+                      int64_t width, int64_t height, int64_t pitch_in, int64_t pitch_out,
+                      int64_t rows_above, int64_t rows_below, int32_t wc, int32_t wr,
+                      void* stream);
+
+/* Iterated stencil: `iterations` passes ping-ponging between d_a (input) and
+ * d_b.  The result lands in d_a when iterations is even, in d_b when odd;
+ * *result_in_b (optional) says which.  Same pitch for both buffers. */
+int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
+                       int64_t height, int64_t pitch, int32_t iterations, int32_t wc,
+                       int32_t wr, void* stream, int32_t* result_in_b);
+
+/* Zero-work legality probe for (wc, wr) on the current device.  Returns
+ * SK_OK (legal), SK_OVERSIZED or SK_REFUSED.  Optional outputs: the
+ * per-kernel maximum block size (cudaFuncAttributes.maxThreadsPerBlock,
+ * replaces kernel_max_wgsize, simoracle.hpp:26), the shared-memory tile bytes
+ * of one pipeline stage, and the load path a launch would take.  Replaces:
+ * simoracle::is_refused (simoracle.hpp:34-35) and ProbeFn (tuner.hpp:17). */
+int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height,
+                     int32_t wc, int32_t wr, int32_t* kernel_max, int64_t* tile_bytes,
+                     int32_t* load_path);
+
+/* Per-kernel maximum workgroup size for the descriptor (replaces
+ * simoracle::kernel_max_wgsize, simoracle.cpp:62-70). */
+int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max);
+
+/* Timed samples of one pass (the sweep's "run", simoracle.cpp:122-141):
+ * `warmup` untimed launches, then `samples` launches each bracketed by a
+ * cudaEvent pair on an internal stream; when flush_l2 != 0 a buffer of
+ * 2 x l2CacheSize is overwritten before every sample.  ms_out[samples]. */
+int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, int64_t width,
+                    int64_t height, int64_t pitch, int32_t wc, int32_t wr, int32_t warmup,
+                    int32_t samples, int32_t flush_l2, double* ms_out);
+
+/* End-to-end call from HOST buffers (the plugin call a SkelCL user makes):
+ * copies h_in (W*H dense) to the device, runs `iterations` passes, copies the
+ * result to h_out.  Device buffers are cached per (size) inside the library. */
+int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,
+                        int64_t width, int64_t height, int32_t iterations, int32_t wc,
+                        int32_t wr);
+
+/* Device features (north-star subsystem 3): the DeviceDescriptor fields of
+ * the reference (scenario.hpp:31-44) read from cudaDeviceProp instead of the
+ * OpenCL device API. */
+typedef struct {
+  char name[128];          /* prop.name + PCI bus id, no '/', ',' or '\n'  */
+  int32_t compute_units;   /* multiProcessorCount                          */
+  int32_t frequency_mhz;   /* cudaDevAttrClockRate / 1000                  */
+  int32_t local_mem_kb;    /* sharedMemPerBlockOptin / 1024                */
+  int32_t global_cache_kb; /* l2CacheSize / 1024                           */
+  int32_t global_mem_mb;   /* totalGlobalMem >> 20                         */
+  int32_t device_max_wgsize; /* maxThreadsPerBlock                         */
+  int32_t simd_width;      /* warpSize                                     */
+  int32_t cc_major, cc_minor;
+  int32_t mem_clock_mhz;
+  int32_t mem_bus_width;
+} sk_device_props;
+
+int sk_device_features(int32_t device, sk_device_props* out);
+
+/* Fill a device buffer with deterministic synthetic input (the reference
+ * Rng stream, rng.hpp:34-72, so CPU and GPU inputs are identical): float
+ * types get 2*uniform01()-1 or uniform01() (kind 0 / 1), int32 gets
+ * uniform01() < 0.5 ? 1 : 0 (kind 2) or floor(256*uniform01()) (kind 3).
+ * Generated on the host and copied. */
+int sk_fill_host(int32_t dtype, int32_t kind, uint64_t seed, void* h_out, int64_t count);
+
+/* Last error text for the calling thread ("" if none). */
+const char* sk_last_error(void);
+
+/* Library version string. */
+const char* sk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SK_STENCIL_H */

@@ -1,0 +1,265 @@
+// B200 stencil executor kernels (sm_100a).
+//
+// K1a  k_stencil_tma      persistent, TMA-pipelined: one elected thread
+//                         streams (tile + border region) boxes into an
+//                         S-stage shared-memory ring with
+//                         cp.async.bulk.tensor.2d + mbarrier complete_tx;
+//                         out-of-bounds box elements arrive zero-filled, which
+//                         is exactly SK_BORDER_PAD with pad 0; other modes
+//                         patch the out-of-range cells of edge tiles in shared
+//                         memory (clamp or pad) before compute.
+// K1b  k_stencil_explicit one tile per block, coalesced loads of the tile with
+//                         the border substitution applied at load time.
+//
+// Both keep the SkelCL execution model: a (wc x wr)
+// workgroup of work-items, one per output cell, computing from a tile of
+// (wc + E + W) x (wr + N + S) elements staged in shared memory.  The block
+// shape is a launch parameter, not a template parameter.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "ops.cuh"
+
+namespace sk {
+
+// Launch geometry, computed on the host (launch.cu) for one (desc, W, H, wc, wr).
+struct Geom {
+  int W, H;                 // computed region (columns, rows)
+  long long pitch_in;       // elements
+  long long pitch_out;      // elements
+  int above, below;         // readable input rows beyond [0, H) (row-shard halos)
+  int N, S, E, Wb;          // border region (Wb = west)
+  int wc, wr;               // workgroup (block) shape
+  int lw;                   // logical tile width  = wc + E + Wb
+  int tile_w;               // smem row pitch (lw padded to 16 B)
+  int tile_h;               // tile rows = wr + N + S
+  int tiles_x, tiles_y;
+  int mode;                 // sk_border_mode
+  int pad_is_zero;          // PAD mode with an all-zero pad value
+  int stage_bytes;          // bytes per pipeline stage (128-aligned)
+  int stages;               // TMA ring depth
+  int box_h, nchunks;       // TMA box height and boxes per tile
+};
+
+// ------------------------------------------------------------------ PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SK_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SK_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ----------------------------------------------------------------- tile view
+template <typename T>
+struct TileView {
+  const T* centre;  // the work-item's own cell in the staged tile
+  int pitch;
+  __device__ __forceinline__ T at(int dr, int dc) const { return centre[dr * pitch + dc]; }
+};
+
+template <typename T>
+__device__ __forceinline__ T pad_value(const T pad) { return pad; }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// True when a tile reaches outside the readable input (needs substitution).
+__device__ __forceinline__ bool tile_is_edge(const Geom& g, int r0, int c0) {
+  return (r0 - g.N < -g.above) || (r0 + g.wr + g.S > g.H + g.below) || (c0 - g.Wb < 0) ||
+         (c0 + g.wc + g.E > g.W);
+}
+
+// Patch the out-of-range cells of an edge tile in shared memory: pad value,
+// or a copy of the nearest in-range cell (which always lies inside the same
+// tile).  Only out-of-range cells are written and only
+// in-range cells are read, so one pass is race-free.
+template <typename T>
+__device__ __forceinline__ void fixup_tile(T* tile, const Geom& g, int r0, int c0, T pad,
+                                           int tid, int nthreads) {
+  const int total = g.tile_h * g.lw;
+  const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
+  for (int i = tid; i < total; i += nthreads) {
+    int tr = i / g.lw;
+    int tc = i - tr * g.lw;
+    int gr = r0 - g.N + tr;
+    int gc = c0 - g.Wb + tc;
+    bool in = gr >= row_lo && gr <= row_hi && gc >= 0 && gc < g.W;
+    if (in) continue;
+    T v;
+    if (g.mode == 0) {
+      v = pad;
+    } else {
+      int cr = clampi(gr, row_lo, row_hi) - (r0 - g.N);
+      int cc = clampi(gc, 0, g.W - 1) - (c0 - g.Wb);
+      v = tile[cr * g.tile_w + cc];
+    }
+    tile[tr * g.tile_w + tc] = v;
+  }
+}
+
+// --------------------------------------------------------------------- K1a
+template <class Op, typename T>
+__device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage, uint64_t* bar,
+                                               const Geom& g, int t) {
+  int ty = t / g.tiles_x;
+  int tx = t - ty * g.tiles_x;
+  int x = tx * g.wc - g.Wb;
+  int y = ty * g.wr - g.N + g.above;  // tensor rows start `above` rows before row 0
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(g.nchunks * g.box_h * g.tile_w * sizeof(T)));
+  for (int k = 0; k < g.nchunks; ++k) {
+    tma_load_2d(stage + k * g.box_h * g.tile_w, map, bar, x, y + k * g.box_h);
+  }
+}
+
+template <class Op, typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT)
+    k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
+                  const T pad, const __grid_constant__ OpParams<T> p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.stages * g.stage_bytes);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nthreads = blockDim.x * blockDim.y;
+  const int ntiles = g.tiles_x * g.tiles_y;
+  const bool fix_edges = !(g.mode == 0 && g.pad_is_zero);
+
+  if (tid == 0) {
+    prefetch_tensormap(&map);
+    for (int s = 0; s < g.stages; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+    for (int s = 0; s < g.stages; ++s) {
+      int t = blockIdx.x + s * gridDim.x;
+      if (t < ntiles) {
+        tma_issue_tile<Op, T>(&map, reinterpret_cast<T*>(smem + s * g.stage_bytes), &bars[s], g,
+                              t);
+      }
+    }
+  }
+  __syncthreads();
+
+  const Op op;
+  int iter = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+    const int s = iter % g.stages;
+    const uint32_t parity = static_cast<uint32_t>((iter / g.stages) & 1);
+    T* tile = reinterpret_cast<T*>(smem + s * g.stage_bytes);
+    const int ty = t / g.tiles_x;
+    const int r0 = ty * g.wr;
+    const int c0 = (t - ty * g.tiles_x) * g.wc;
+
+    mbar_wait_parity(&bars[s], parity);
+    if (fix_edges && tile_is_edge(g, r0, c0)) {
+      fixup_tile(tile, g, r0, c0, pad, tid, nthreads);
+      fence_proxy_async_smem();  // generic writes before the next async refill
+      __syncthreads();
+    }
+
+    const int r = r0 + threadIdx.y;
+    const int c = c0 + threadIdx.x;
+    TileView<T> view{tile + (threadIdx.y + g.N) * g.tile_w + threadIdx.x + g.Wb, g.tile_w};
+    T res = op.template apply<T>(view, p);
+    __syncthreads();  // every work-item has read stage s
+    if (tid == 0) {
+      int tn = t + g.stages * gridDim.x;
+      if (tn < ntiles) tma_issue_tile<Op, T>(&map, tile, &bars[s], g, tn);
+    }
+    if (r < g.H && c < g.W) out[static_cast<long long>(r) * g.pitch_out + c] = res;
+  }
+}
+
+// --------------------------------------------------------------------- K1b
+template <class Op, typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT)
+    k_stencil_explicit(const T* __restrict__ in, T* __restrict__ out, const Geom g, const T pad,
+                       const __grid_constant__ OpParams<T> p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* tile = reinterpret_cast<T*>(smem);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nthreads = blockDim.x * blockDim.y;
+  const int r0 = blockIdx.y * g.wr;
+  const int c0 = blockIdx.x * g.wc;
+  const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
+  const int total = g.tile_h * g.lw;
+
+  if (!tile_is_edge(g, r0, c0)) {
+    for (int i = tid; i < total; i += nthreads) {
+      int tr = i / g.lw;
+      int tc = i - tr * g.lw;
+      tile[tr * g.tile_w + tc] =
+          in[static_cast<long long>(r0 - g.N + tr) * g.pitch_in + (c0 - g.Wb + tc)];
+    }
+  } else {
+    for (int i = tid; i < total; i += nthreads) {
+      int tr = i / g.lw;
+      int tc = i - tr * g.lw;
+      int gr = r0 - g.N + tr;
+      int gc = c0 - g.Wb + tc;
+      T v;
+      if (gr >= row_lo && gr <= row_hi && gc >= 0 && gc < g.W) {
+        v = in[static_cast<long long>(gr) * g.pitch_in + gc];
+      } else if (g.mode == 0) {
+        v = pad;
+      } else {
+        v = in[static_cast<long long>(clampi(gr, row_lo, row_hi)) * g.pitch_in +
+               clampi(gc, 0, g.W - 1)];
+      }
+      tile[tr * g.tile_w + tc] = v;
+    }
+  }
+  __syncthreads();
+
+  const int r = r0 + threadIdx.y;
+  const int c = c0 + threadIdx.x;
+  if (r < g.H && c < g.W) {
+    const Op op;
+    TileView<T> view{tile + (threadIdx.y + g.N) * g.tile_w + threadIdx.x + g.Wb, g.tile_w};
+    out[static_cast<long long>(r) * g.pitch_out + c] = op.template apply<T>(view, p);
+  }
+}
+
+}  // namespace sk

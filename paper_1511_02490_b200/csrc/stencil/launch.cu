@@ -1,0 +1,708 @@
+// Host side of the B200 stencil executor: geometry, legality (refusal),
+// TMA tensor-map cache, kernel dispatch and the extern "C" ABI declared in
+// include/sk_stencil.h.
+//
+// Legality mirrors the reference's constraint model (space.hpp:38-51,
+// simoracle.cpp:62-88) with real device facts instead of simulated ones:
+//   oversized  <=> wc*wr > min(maxThreadsPerBlock, cudaFuncAttributes.maxThreadsPerBlock)
+//   refused    <=> the staged tile does not fit the opt-in shared memory, no
+//                  block can be resident, or the launch reports a
+//                  (non-sticky) configuration/resource error.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.cuh"
+#include "sk_stencil.h"
+
+namespace sk {
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+// Launch-time errors that leave the context usable and mean "this
+// configuration cannot run" -> refused parameter.
+bool is_config_error(cudaError_t e) {
+  return e == cudaErrorInvalidConfiguration || e == cudaErrorLaunchOutOfResources ||
+         e == cudaErrorInvalidValue ||
+         e == cudaErrorSharedObjectInitFailed;
+}
+
+size_t dtype_size(int dtype) { return dtype == SK_FLOAT64 ? 8 : 4; }
+
+struct DeviceInfo {
+  int sms = 0;
+  int max_threads = 0;
+  int smem_optin = 0;
+  int smem_per_sm = 0;
+  int l2_bytes = 0;
+};
+
+std::mutex g_mu;
+std::map<int, DeviceInfo> g_devices;
+
+int current_device_info(DeviceInfo* out, int* dev_out = nullptr) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  if (dev_out) *dev_out = dev;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_devices.find(dev);
+  if (it == g_devices.end()) {
+    DeviceInfo d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.max_threads, cudaDevAttrMaxThreadsPerBlock, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&d.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&d.l2_bytes, cudaDevAttrL2CacheSize, dev);
+    e = cudaGetLastError();
+    if (e != cudaSuccess || d.sms == 0) {
+      return fail(SK_ECUDA, "device attribute query failed: %s", cudaGetErrorString(e));
+    }
+    it = g_devices.emplace(dev, d).first;
+  }
+  *out = it->second;
+  return SK_OK;
+}
+
+// ------------------------------------------------------------ op parameters
+long long binom(int n, int k) {
+  long long r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+template <typename T>
+void fill_params(const sk_stencil_desc& d, OpParams<T>* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->north = d.north;
+  p->south = d.south;
+  p->east = d.east;
+  p->west = d.west;
+  p->complexity = d.complexity;
+  // Synthetic kernels: instruction budget -> dependent ALU steps per cell
+  // (DESIGN.md §3.9): heavy (synthetic-b) instructions/4, light instructions/32.
+  p->alu_iters = d.op == SK_OP_SYNTHETIC ? (d.complexity ? d.instructions / 4 : d.instructions / 32)
+                                         : 0;
+  if (d.op == SK_OP_GAUSSIAN) {
+    int g = d.north;
+    p->gauss_radius = g;
+    int n = 2 * g + 1;
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) {
+        long long cij = binom(2 * g, i) * binom(2 * g, j);
+        if constexpr (std::is_same_v<T, int32_t>) {
+          p->gauss_w[i * n + j] = cij;
+        } else {
+          p->gauss_w[i * n + j] = static_cast<T>(std::ldexp(static_cast<double>(cij), -4 * g));
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------- descriptor checks
+int validate_desc(const sk_stencil_desc* d) {
+  if (!d) return fail(SK_EINVAL, "null descriptor");
+  if (d->op < 0 || d->op >= SK_OP_COUNT) return fail(SK_EINVAL, "bad op %d", d->op);
+  if (d->dtype < SK_INT32 || d->dtype > SK_FLOAT64) return fail(SK_EINVAL, "bad dtype %d", d->dtype);
+  if (d->border_mode != SK_BORDER_PAD && d->border_mode != SK_BORDER_NEAREST) {
+    return fail(SK_EINVAL, "bad border mode %d", d->border_mode);
+  }
+  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_EXPLICIT) {
+    return fail(SK_EINVAL, "bad load path %d", d->load_path);
+  }
+  for (int b : {d->north, d->south, d->east, d->west}) {
+    if (b < 0 || b > 64) return fail(SK_EINVAL, "border values must be in [0, 64]");
+  }
+  int need = 0;
+  switch (d->op) {
+    case SK_OP_FIVE_POINT: case SK_OP_HEAT: case SK_OP_GOL: case SK_OP_SOBEL: case SK_OP_NMS:
+      need = 1;
+      break;
+    case SK_OP_GAUSSIAN:
+      if (d->north < 1 || d->north > 10 || d->south != d->north || d->east != d->north ||
+          d->west != d->north) {
+        return fail(SK_EINVAL, "gaussian needs equal borders g in [1, 10]");
+      }
+      break;
+    case SK_OP_SYNTHETIC:
+      if (d->instructions < 1) return fail(SK_EINVAL, "synthetic needs instructions >= 1");
+      break;
+    default:
+      break;
+  }
+  if (need && (d->north < need || d->south < need || d->east < need || d->west < need)) {
+    return fail(SK_EINVAL, "op %d needs borders >= %d in every direction", d->op, need);
+  }
+  return SK_OK;
+}
+
+// --------------------------------------------------------- kernel registry
+using KernelPtr = const void*;
+
+struct KernelPair {
+  KernelPtr tma;
+  KernelPtr explicit_;
+};
+
+template <class Op, typename T>
+KernelPair kernels_for() {
+  return {reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1024>),
+          reinterpret_cast<KernelPtr>(&k_stencil_explicit<Op, T, 1024>)};
+}
+
+template <typename T>
+KernelPair kernels_for_op(const sk_stencil_desc& d) {
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return kernels_for<FivePoint, T>();
+    case SK_OP_HEAT: return kernels_for<Heat, T>();
+    case SK_OP_GOL: return kernels_for<Gol, T>();
+    case SK_OP_BOXMEAN:
+      if (d.north == 5 && d.south == 1 && d.east == 3 && d.west == 0) {
+        return kernels_for<BoxMeanFixed<5, 1, 3, 0>, T>();
+      }
+      return kernels_for<BoxMean, T>();
+    case SK_OP_GAUSSIAN: return kernels_for<Gaussian, T>();
+    case SK_OP_SOBEL: return kernels_for<Sobel, T>();
+    case SK_OP_NMS: return kernels_for<Nms, T>();
+    case SK_OP_THRESHOLD: return kernels_for<Threshold, T>();
+    case SK_OP_SYNTHETIC: return kernels_for<Synthetic, T>();
+  }
+  return {nullptr, nullptr};
+}
+
+KernelPair kernels_for_desc(const sk_stencil_desc& d) {
+  switch (d.dtype) {
+    case SK_INT32: return kernels_for_op<int32_t>(d);
+    case SK_FLOAT32: return kernels_for_op<float>(d);
+    default: return kernels_for_op<double>(d);
+  }
+}
+
+// Per-(device, kernel) attributes: kernel max threads and the opt-in smem
+// attribute, set once.
+struct KernelAttr {
+  int max_threads = 0;
+  int max_dyn_smem = 0;
+};
+std::map<std::pair<int, KernelPtr>, KernelAttr> g_kattr;
+
+int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, k);
+  auto it = g_kattr.find(key);
+  if (it == g_kattr.end()) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) {
+      return fail(SK_ECUDA, "cudaFuncGetAttributes: %s", cudaGetErrorString(e));
+    }
+    KernelAttr a;
+    a.max_threads = fa.maxThreadsPerBlock;
+    a.max_dyn_smem = info.smem_optin - static_cast<int>(fa.sharedSizeBytes);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.max_dyn_smem);
+    if (e != cudaSuccess) {
+      return fail(SK_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
+    it = g_kattr.emplace(key, a).first;
+  }
+  *out = it->second;
+  return SK_OK;
+}
+
+std::map<std::tuple<int, KernelPtr, int, int>, int> g_occ;
+
+int occupancy(int dev, KernelPtr k, int threads, int smem) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find({dev, k, threads, smem});
+    if (it != g_occ.end()) return it->second;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_occ[{dev, k, threads, smem}] = n;
+  return n;
+}
+
+// ------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<EncodeTiledFn>(nullptr);
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+struct MapKey {
+  int dev;
+  const void* base;
+  int dtype;
+  long long w, h, pitch;
+  int box_w, box_h;
+  bool operator<(const MapKey& o) const {
+    return std::tie(dev, base, dtype, w, h, pitch, box_w, box_h) <
+           std::tie(o.dev, o.base, o.dtype, o.w, o.h, o.pitch, o.box_w, o.box_h);
+  }
+};
+std::map<MapKey, CUtensorMap> g_maps;
+
+int tensor_map(const MapKey& key, CUtensorMap* out) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return SK_OK;
+    }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMapDataType dt = key.dtype == SK_INT32     ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                           : key.dtype == SK_FLOAT32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(key.w), static_cast<cuuint64_t>(key.h)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(key.pitch) * dtype_size(key.dtype)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(key.box_w), static_cast<cuuint32_t>(key.box_h)};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, dt, 2, const_cast<void*>(key.base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = m;
+  *out = m;
+  return SK_OK;
+}
+
+// ------------------------------------------------------------------ plan
+struct Plan {
+  Geom g{};
+  KernelPtr kernel = nullptr;
+  bool tma = false;
+  int threads = 0;
+  int smem = 0;
+  int grid = 0;
+  int kernel_max = 0;
+  long long tile_bytes = 0;
+};
+
+// Builds the launch plan; returns SK_OK, SK_OVERSIZED, SK_REFUSED or an error.
+// `in` may be null for a probe (TMA eligibility then assumes aligned buffers).
+int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
+              long long pitch_out, long long above, long long below, int wc, int wr,
+              const void* in, Plan* plan) {
+  if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) {
+    return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
+  }
+  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
+  if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
+  DeviceInfo info;
+  int dev = 0;
+  if (int rc = current_device_info(&info, &dev)) return rc;
+  KernelPair kp = kernels_for_desc(d);
+  KernelAttr a_tma, a_exp;
+  if (int rc = kernel_attr(dev, kp.tma, info, &a_tma)) return rc;
+  if (int rc = kernel_attr(dev, kp.explicit_, info, &a_exp)) return rc;
+
+  const long long threads = static_cast<long long>(wc) * wr;
+  const size_t es = dtype_size(d.dtype);
+  Geom& g = plan->g;
+  g.W = static_cast<int>(W);
+  g.H = static_cast<int>(H);
+  g.pitch_in = pitch_in;
+  g.pitch_out = pitch_out;
+  g.above = static_cast<int>(std::min<long long>(above, d.north));
+  g.below = static_cast<int>(std::min<long long>(below, d.south));
+  g.N = d.north;
+  g.S = d.south;
+  g.E = d.east;
+  g.Wb = d.west;
+  g.wc = wc;
+  g.wr = wr;
+  g.lw = wc + d.east + d.west;
+  const int vec = static_cast<int>(16 / es);
+  g.tile_w = (g.lw + vec - 1) / vec * vec;
+  g.tile_h = wr + d.north + d.south;
+  g.tiles_x = static_cast<int>((W + wc - 1) / wc);
+  g.tiles_y = static_cast<int>((H + wr - 1) / wr);
+  g.mode = d.border_mode;
+  g.pad_is_zero = d.pad_value == 0.0 && !std::signbit(d.pad_value);
+  plan->tile_bytes = static_cast<long long>(g.lw) * g.tile_h * static_cast<long long>(es);
+
+  // TMA eligibility: box width <= 256 elements, 16-B aligned base and pitch.
+  bool tma_ok = g.tile_w <= 256 && (pitch_in * es) % 16 == 0 &&
+                (in == nullptr || (reinterpret_cast<uintptr_t>(in) % 16) == 0) &&
+                static_cast<long long>(g.tiles_x) * g.tiles_y < (1LL << 31);
+  bool use_tma = d.load_path == SK_LOAD_TMA || (d.load_path == SK_LOAD_AUTO && tma_ok);
+  if (d.load_path == SK_LOAD_TMA && !tma_ok) {
+    return fail(SK_ENOTSUP, "TMA path not possible for this tile/buffer (tile_w %d)", g.tile_w);
+  }
+  const KernelAttr& attr = use_tma ? a_tma : a_exp;
+  plan->kernel_max = std::min(info.max_threads, attr.max_threads);
+  plan->threads = static_cast<int>(threads);
+  if (threads > plan->kernel_max) {
+    return fail(SK_OVERSIZED, "workgroup %dx%d exceeds the effective maximum %d", wc, wr,
+                plan->kernel_max);
+  }
+  plan->tma = use_tma;
+  plan->kernel = use_tma ? kp.tma : kp.explicit_;
+
+  if (!use_tma) {
+    long long smem = static_cast<long long>(g.tile_w) * g.tile_h * static_cast<long long>(es);
+    if (smem > attr.max_dyn_smem) {
+      return fail(SK_REFUSED, "tile %lld B exceeds shared memory %d B", smem, attr.max_dyn_smem);
+    }
+    g.stages = 1;
+    g.stage_bytes = static_cast<int>(smem);
+    g.box_h = g.tile_h;
+    g.nchunks = 1;
+    plan->smem = static_cast<int>(smem);
+    if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
+      return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
+    }
+    plan->grid = 0;  // 2-D grid (tiles_x, tiles_y)
+    return SK_OK;
+  }
+
+  g.nchunks = (g.tile_h + 255) / 256;
+  g.box_h = (g.tile_h + g.nchunks - 1) / g.nchunks;
+  long long stage = static_cast<long long>(g.tile_w) * g.box_h * g.nchunks *
+                    static_cast<long long>(es);
+  stage = (stage + 127) / 128 * 128;
+  if (stage + 64 > attr.max_dyn_smem) {
+    return fail(SK_REFUSED, "tile %lld B exceeds shared memory %d B", stage, attr.max_dyn_smem);
+  }
+  g.stage_bytes = static_cast<int>(stage);
+  // Ring depth: as deep as the per-block share of the SM's shared memory
+  // allows at the thread-limited occupancy, between 2 and 8 stages.
+  int occ2 = occupancy(dev, plan->kernel, plan->threads,
+                       static_cast<int>(std::min<long long>(2 * stage + 64, attr.max_dyn_smem)));
+  int blocks = std::max(1, occ2);
+  long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 64;
+  int stages = static_cast<int>(std::clamp<long long>(share / stage, 1, 8));
+  while (stages > 1 && stage * stages + 64 > attr.max_dyn_smem) --stages;
+  g.stages = stages;
+  plan->smem = static_cast<int>(stage * stages + 64);
+  int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem);
+  if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
+  long long ntiles = static_cast<long long>(g.tiles_x) * g.tiles_y;
+  plan->grid = static_cast<int>(std::min<long long>(ntiles, static_cast<long long>(occ) * info.sms));
+  return SK_OK;
+}
+
+template <typename T>
+int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, void* out,
+                 long long above_rows, long long H_total_rows, cudaStream_t stream) {
+  OpParams<T> p;
+  fill_params<T>(d, &p);
+  T pad = static_cast<T>(d.pad_value);
+  dim3 block(plan.g.wc, plan.g.wr, 1);
+  cudaError_t e;
+  if (plan.tma) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    MapKey key{dev,
+               static_cast<const char*>(in) -
+                   above_rows * plan.g.pitch_in * static_cast<long long>(sizeof(T)),
+               d.dtype,
+               plan.g.W,
+               H_total_rows,
+               plan.g.pitch_in,
+               plan.g.tile_w,
+               plan.g.box_h};
+    CUtensorMap map;
+    if (int rc = tensor_map(key, &map)) return rc;
+    void* args[] = {&map, &out, const_cast<Geom*>(&plan.g), &pad, &p};
+    e = cudaLaunchKernel(plan.kernel, dim3(plan.grid), block, args, plan.smem, stream);
+  } else {
+    const T* tin = static_cast<const T*>(in);
+    T* tout = static_cast<T*>(out);
+    void* args[] = {&tin, &tout, const_cast<Geom*>(&plan.g), &pad, &p};
+    e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x, plan.g.tiles_y), block, args,
+                         plan.smem, stream);
+  }
+  if (e != cudaSuccess) {
+    if (is_config_error(e)) {
+      cudaGetLastError();
+      return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
+    }
+    return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  }
+  return SK_OK;
+}
+
+int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
+           long long pitch_in, long long pitch_out, long long above, long long below, int wc,
+           int wr, cudaStream_t stream) {
+  Plan plan;
+  if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan)) {
+    return rc;
+  }
+  long long used_above = plan.g.above;
+  long long total_rows = H + plan.g.above + plan.g.below;
+  switch (d.dtype) {
+    case SK_INT32:
+      return launch_typed<int32_t>(d, plan, in, out, used_above, total_rows, stream);
+    case SK_FLOAT32:
+      return launch_typed<float>(d, plan, in, out, used_above, total_rows, stream);
+    default:
+      return launch_typed<double>(d, plan, in, out, used_above, total_rows, stream);
+  }
+}
+
+// ------------------------------------------------------------- scratch
+struct Scratch {
+  void* flush = nullptr;
+  size_t flush_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* host_in = nullptr;
+  void* host_out = nullptr;
+  void* dev_a = nullptr;
+  void* dev_b = nullptr;
+  size_t dev_bytes = 0;
+};
+std::map<int, Scratch> g_scratch;
+
+int scratch(Scratch** out) {
+  DeviceInfo info;
+  int dev = 0;
+  if (int rc = current_device_info(&info, &dev)) return rc;
+  std::lock_guard<std::mutex> lk(g_mu);
+  Scratch& s = g_scratch[dev];
+  if (!s.stream) {
+    if (cudaStreamCreate(&s.stream) != cudaSuccess || cudaEventCreate(&s.ev0) != cudaSuccess ||
+        cudaEventCreate(&s.ev1) != cudaSuccess) {
+      return fail(SK_ECUDA, "stream/event creation failed");
+    }
+    s.flush_bytes = static_cast<size_t>(info.l2_bytes) * 2;
+    if (cudaMalloc(&s.flush, s.flush_bytes) != cudaSuccess) {
+      return fail(SK_ECUDA, "L2 flush buffer allocation failed");
+    }
+  }
+  *out = &s;
+  return SK_OK;
+}
+
+}  // namespace
+}  // namespace sk
+
+// ======================================================================= ABI
+using namespace sk;
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+
+const char* sk_version(void) { return "sk_stencil 0.1 sm_100a"; }
+
+int sk_stencil_launch(const sk_stencil_desc* desc, const void* d_in, void* d_out, int64_t width,
+                      int64_t height, int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
+                      int64_t rows_below, int32_t wc, int32_t wr, void* stream) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!d_in || !d_out) return fail(SK_EINVAL, "null buffer");
+  if (rows_above < 0 || rows_below < 0) return fail(SK_EINVAL, "negative halo rows");
+  return launch(*desc, d_in, d_out, width, height, pitch_in, pitch_out, rows_above, rows_below,
+                wc, wr, static_cast<cudaStream_t>(stream));
+}
+
+int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
+                       int64_t height, int64_t pitch, int32_t iterations, int32_t wc,
+                       int32_t wr, void* stream, int32_t* result_in_b) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!d_a || !d_b) return fail(SK_EINVAL, "null buffer");
+  if (iterations < 0) return fail(SK_EINVAL, "negative iterations");
+  void* src = d_a;
+  void* dst = d_b;
+  for (int i = 0; i < iterations; ++i) {
+    if (int rc = launch(*desc, src, dst, width, height, pitch, pitch, 0, 0, wc, wr,
+                        static_cast<cudaStream_t>(stream))) {
+      return rc;
+    }
+    std::swap(src, dst);
+  }
+  if (result_in_b) *result_in_b = (iterations % 2) == 1;
+  return SK_OK;
+}
+
+int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height, int32_t wc,
+                     int32_t wr, int32_t* kernel_max, int64_t* tile_bytes, int32_t* load_path) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  Plan plan;
+  int rc = make_plan(*desc, width, height, width, width, 0, 0, wc, wr, nullptr, &plan);
+  if (kernel_max) *kernel_max = plan.kernel_max;
+  if (tile_bytes) *tile_bytes = plan.tile_bytes;
+  if (load_path) *load_path = plan.tma ? SK_LOAD_TMA : SK_LOAD_EXPLICIT;
+  return rc;
+}
+
+int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!kernel_max) return fail(SK_EINVAL, "null output");
+  Plan plan;
+  // A 2x2 block on a small grid is always within the maxima; the plan
+  // carries the per-kernel maximum of the path AUTO would take.
+  int rc = make_plan(*desc, 64, 64, 64, 64, 0, 0, 2, 2, nullptr, &plan);
+  if (rc == SK_OK || rc == SK_REFUSED || rc == SK_OVERSIZED) {
+    *kernel_max = plan.kernel_max;
+    return SK_OK;
+  }
+  return rc;
+}
+
+int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, int64_t width,
+                    int64_t height, int64_t pitch, int32_t wc, int32_t wr, int32_t warmup,
+                    int32_t samples, int32_t flush_l2, double* ms_out) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!d_in || !d_out || (samples > 0 && !ms_out)) return fail(SK_EINVAL, "null argument");
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  for (int i = 0; i < warmup; ++i) {
+    if (int rc = launch(*desc, d_in, d_out, width, height, pitch, pitch, 0, 0, wc, wr, s->stream)) {
+      return rc;
+    }
+  }
+  for (int i = 0; i < samples; ++i) {
+    if (flush_l2) cudaMemsetAsync(s->flush, i & 0xff, s->flush_bytes, s->stream);
+    cudaEventRecord(s->ev0, s->stream);
+    if (int rc = launch(*desc, d_in, d_out, width, height, pitch, pitch, 0, 0, wc, wr, s->stream)) {
+      return rc;
+    }
+    cudaEventRecord(s->ev1, s->stream);
+    cudaError_t e = cudaEventSynchronize(s->ev1);
+    if (e != cudaSuccess) return fail(SK_ECUDA, "sample failed: %s", cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+    ms_out[i] = ms;
+  }
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "timing stream failed: %s", cudaGetErrorString(e));
+  return SK_OK;
+}
+
+int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,
+                        int64_t width, int64_t height, int32_t iterations, int32_t wc,
+                        int32_t wr) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!h_in || !h_out) return fail(SK_EINVAL, "null host buffer");
+  if (width < 1 || height < 1) return fail(SK_EINVAL, "bad dims");
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  size_t bytes = static_cast<size_t>(width) * height * dtype_size(desc->dtype);
+  if (s->dev_bytes < bytes) {
+    cudaFree(s->dev_a);
+    cudaFree(s->dev_b);
+    s->dev_a = s->dev_b = nullptr;
+    s->dev_bytes = 0;
+    if (cudaMalloc(&s->dev_a, bytes) != cudaSuccess || cudaMalloc(&s->dev_b, bytes) != cudaSuccess) {
+      return fail(SK_ECUDA, "device buffer allocation failed (%zu B)", bytes);
+    }
+    s->dev_bytes = bytes;
+  }
+  cudaMemcpyAsync(s->dev_a, h_in, bytes, cudaMemcpyHostToDevice, s->stream);
+  int32_t in_b = 0;
+  if (int rc = sk_stencil_iterate(desc, s->dev_a, s->dev_b, width, height, width, iterations, wc,
+                                  wr, s->stream, &in_b)) {
+    return rc;
+  }
+  cudaMemcpyAsync(h_out, in_b ? s->dev_b : s->dev_a, bytes, cudaMemcpyDeviceToHost, s->stream);
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "run_host failed: %s", cudaGetErrorString(e));
+  return SK_OK;
+}
+
+int sk_device_features(int32_t device, sk_device_props* out) {
+  g_last_error.clear();
+  if (!out) return fail(SK_EINVAL, "null output");
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  std::memset(out, 0, sizeof(*out));
+  std::string name = std::string(p.name) + "-" + std::to_string(p.pciBusID);
+  for (char& ch : name) {
+    if (ch == '/' || ch == ',' || ch == '\n' || ch == ' ') ch = '-';
+  }
+  std::snprintf(out->name, sizeof out->name, "%s", name.c_str());
+  int clock_khz = 0, mem_khz = 0;
+  cudaDeviceGetAttribute(&clock_khz, cudaDevAttrClockRate, device);
+  cudaDeviceGetAttribute(&mem_khz, cudaDevAttrMemoryClockRate, device);
+  out->compute_units = p.multiProcessorCount;
+  out->frequency_mhz = clock_khz / 1000;
+  out->local_mem_kb = static_cast<int32_t>(p.sharedMemPerBlockOptin / 1024);
+  out->global_cache_kb = p.l2CacheSize / 1024;
+  out->global_mem_mb = static_cast<int32_t>(p.totalGlobalMem >> 20);
+  out->device_max_wgsize = p.maxThreadsPerBlock;
+  out->simd_width = p.warpSize;
+  out->cc_major = p.major;
+  out->cc_minor = p.minor;
+  out->mem_clock_mhz = mem_khz / 1000;
+  out->mem_bus_width = p.memoryBusWidth;
+  return SK_OK;
+}
+
+int sk_fill_host(int32_t dtype, int32_t kind, uint64_t seed, void* h_out, int64_t count) {
+  g_last_error.clear();
+  if (!h_out || count < 0) return fail(SK_EINVAL, "bad fill arguments");
+  std::mt19937_64 eng(seed);  // the reference Rng engine (rng.hpp:34-72)
+  auto u01 = [&]() { return static_cast<double>(eng() >> 11) * 0x1.0p-53; };
+  for (int64_t i = 0; i < count; ++i) {
+    double u = u01();
+    double v = kind == 0 ? 2.0 * u - 1.0 : kind == 1 ? u : kind == 2 ? (u < 0.5 ? 1.0 : 0.0)
+                                                                      : std::floor(256.0 * u);
+    switch (dtype) {
+      case SK_INT32: static_cast<int32_t*>(h_out)[i] = static_cast<int32_t>(v); break;
+      case SK_FLOAT32: static_cast<float*>(h_out)[i] = static_cast<float>(v); break;
+      case SK_FLOAT64: static_cast<double*>(h_out)[i] = v; break;
+      default: return fail(SK_EINVAL, "bad dtype");
+    }
+  }
+  return SK_OK;
+}
+
+}  // extern "C"

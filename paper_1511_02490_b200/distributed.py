@@ -1,0 +1,131 @@
+"""Row-block decomposition of iterated stencils over P ranks (north-star
+subsystem 5).
+
+Rank p owns global rows [p*H/P, (p+1)*H/P) and keeps them in a buffer of
+N + rows + S rows: N north-halo rows, the owned rows, S south-halo rows.
+Per iteration, inside one batched P2P group:
+
+    send my first S owned rows  -> p-1   (its south halo)
+    recv my north halo (N rows) <- p-1
+    send my last N owned rows   -> p+1   (its north halo)
+    recv my south halo (S rows) <- p+1
+
+Row-major storage makes every message a contiguous slice (no packing).  The
+global edges (rank 0's north, rank P-1's south) have no halo: the launch
+passes rows_above = 0 / rows_below = 0 there and the executor applies the
+border mode (pad or nearest) exactly as the single-GPU pass does, so the
+decomposed run is bit-identical to the undivided one.
+
+Transport is torch.distributed point-to-point (NCCL over NVLink on B200,
+gloo on CPU for the multi-process tests).  The per-iteration compute is a
+callable so the same exchange logic drives the CUDA executor in production
+and the CPU oracle in tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class RowShard:
+    height: int   # global rows
+    width: int
+    rank: int
+    world: int
+    north: int
+    south: int
+
+    @property
+    def r0(self) -> int:
+        return self.rank * self.height // self.world
+
+    @property
+    def r1(self) -> int:
+        return (self.rank + 1) * self.height // self.world
+
+    @property
+    def rows(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def rows_above(self) -> int:
+        """Halo rows that hold real data above the owned rows."""
+        return self.north if self.rank > 0 else 0
+
+    @property
+    def rows_below(self) -> int:
+        return self.south if self.rank < self.world - 1 else 0
+
+    @property
+    def buffer_rows(self) -> int:
+        return self.north + self.rows + self.south
+
+    def check(self) -> None:
+        if self.rows < max(self.north, self.south, 1):
+            raise ValueError(f"rank {self.rank} owns {self.rows} rows; halos need "
+                             f">= max(N={self.north}, S={self.south})")
+
+    def owned(self, buf: torch.Tensor) -> torch.Tensor:
+        return buf[self.north:self.north + self.rows]
+
+
+def exchange_halos(buf: torch.Tensor, shard: RowShard, group=None) -> None:
+    """Fill the north/south halo rows of `buf` from the neighbouring ranks."""
+    n, s, h = shard.north, shard.south, shard.rows
+    ops = []
+    if shard.rank > 0:
+        prev = shard.rank - 1
+        if s:
+            ops.append(dist.P2POp(dist.isend, buf[n:n + s], prev, group))
+        if n:
+            ops.append(dist.P2POp(dist.irecv, buf[0:n], prev, group))
+    if shard.rank < shard.world - 1:
+        nxt = shard.rank + 1
+        if n:
+            ops.append(dist.P2POp(dist.isend, buf[n + h - n:n + h], nxt, group))
+        if s:
+            ops.append(dist.P2POp(dist.irecv, buf[n + h:n + h + s], nxt, group))
+    if ops:
+        for work in dist.batch_isend_irecv(ops):
+            work.wait()
+
+
+StepFn = Callable[[torch.Tensor, torch.Tensor, RowShard], None]
+"""step(src_buf, dst_buf, shard): one stencil pass from src's owned rows (with
+shard.rows_above / rows_below halo rows readable around them) into dst's
+owned rows."""
+
+
+def iterate_sharded(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iterations: int,
+                    step: StepFn, group=None) -> torch.Tensor:
+    """`iterations` exchange+pass rounds ping-ponging a/b; returns the buffer
+    holding the result (owned rows are shard.owned(result))."""
+    shard.check()
+    src, dst = a, b
+    for _ in range(iterations):
+        if shard.world > 1:
+            exchange_halos(src, shard, group)
+        step(src, dst, shard)
+        src, dst = dst, src
+    return src
+
+
+def cuda_step(stencil, wc: int, wr: int) -> StepFn:
+    """Production step: one sm_100a executor launch on the current stream."""
+
+    def step(src: torch.Tensor, dst: torch.Tensor, shard: RowShard) -> None:
+        stencil(src[shard.north:], dst[shard.north:], wc, wr, rows_above=shard.rows_above,
+                rows_below=shard.rows_below, height=shard.rows)
+
+    return step
+
+
+def scatter_rows(full: torch.Tensor, shard: RowShard) -> torch.Tensor:
+    """Buffer for `shard` initialised from the global grid (halos zero)."""
+    buf = torch.zeros((shard.buffer_rows, shard.width), dtype=full.dtype, device=full.device)
+    buf[shard.north:shard.north + shard.rows] = full[shard.r0:shard.r1]
+    return buf

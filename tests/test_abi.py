@@ -1,0 +1,60 @@
+"""The C-ABI library loads without a GPU and exports every symbol declared in
+include/sk_stencil.h (no compute calls here)."""
+from __future__ import annotations
+
+import ctypes
+
+import pytest
+
+from paper_1511_02490_b200 import _native as N
+
+
+def test_library_exports_every_header_symbol():
+    lib = N.lib()
+    syms = N.header_symbols()
+    assert len(syms) >= 10
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, f"missing exports: {missing}"
+
+
+def test_prototypes_cover_header():
+    assert set(N.header_symbols()) == set(N._PROTOTYPES)
+
+
+def test_descriptor_layout_matches_header():
+    # int32 x7, double, int32 x3 with natural alignment -> 56 bytes
+    assert ctypes.sizeof(N.sk_stencil_desc) == 56
+    assert N.sk_stencil_desc.pad_value.offset == 32
+
+
+def test_version_and_error_strings():
+    assert N.lib().sk_version().decode().startswith("sk_stencil")
+    assert isinstance(N.last_error(), str)
+
+
+def test_fill_host_matches_reference_rng():
+    # uniform01 = (mt19937_64() >> 11) * 2^-53 (rng.hpp:48) -> kind 1 (float64)
+    import numpy as np
+
+    from paper_1511_02490_b200 import fill_host
+
+    a = np.empty(5, np.float64)
+    fill_host(a, 1, 5489)
+    # std::mt19937_64 default seed 5489: first output 14514284786278117030
+    assert a[0] == (14514284786278117030 >> 11) * 2.0 ** -53
+
+
+def test_invalid_descriptor_is_einval_without_gpu():
+    d = N.sk_stencil_desc(op=99, dtype=1)
+    km = ctypes.c_int32(0)
+    rc = N.lib().sk_kernel_max_wgsize(ctypes.byref(d), ctypes.byref(km))
+    assert rc == N.SK_EINVAL
+
+
+@pytest.mark.parametrize("field,value", [("dtype", 7), ("border_mode", 3), ("north", 65),
+                                         ("load_path", 9)])
+def test_bad_fields_rejected(field, value):
+    d = N.sk_stencil_desc(op=0, dtype=1, north=1, south=1, east=1, west=1)
+    setattr(d, field, value)
+    rc = N.lib().sk_stencil_launch(ctypes.byref(d), 1, 1, 8, 8, 8, 8, 0, 0, 2, 2, None)
+    assert rc == N.SK_EINVAL

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a executor vs the CPU oracle (and the numpy golden
+fixtures), through the C-ABI.  Bit-exact for every dtype (fp32/fp64 are
+compiled without FMA contraction on both sides); the north-star tolerance for
+fp32 (1e-5 relative) is asserted as well so a contraction regression is
+reported with its size."""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1511_02490_b200 import IllegalWorkgroupSize, RefusedParameter, Stencil  # noqa: E402
+
+GOLDEN = Path(__file__).resolve().parent / "golden" / "stencil_golden.npz"
+TDT = {"int32": torch.int32, "float32": torch.float32, "float64": torch.float64}
+FP32_RTOL = 1e-5
+
+
+def to_dev(x: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def gpu_pass(st: Stencil, x: np.ndarray, wc: int, wr: int) -> np.ndarray:
+    a = to_dev(x)
+    b = torch.empty_like(a)
+    st(a, b, wc, wr)
+    torch.cuda.synchronize()
+    return b.cpu().numpy()
+
+
+def assert_same(got: np.ndarray, want: np.ndarray, what: str):
+    assert got.dtype == want.dtype
+    if got.dtype == np.float32:
+        np.testing.assert_allclose(got, want, rtol=FP32_RTOL, atol=1e-6, err_msg=what)
+    assert got.tobytes() == want.tobytes(), f"{what}: not bit-identical to the oracle"
+
+
+def rand_grid(dtype, shape, seed, op="x"):
+    rng = np.random.default_rng(seed)
+    if dtype == "int32":
+        if op == "gol":
+            return (rng.random(shape) < 0.45).astype(np.int32)
+        return rng.integers(-1000, 1000, size=shape, dtype=np.int32)
+    return (2 * rng.random(shape) - 1).astype(dtype)
+
+
+SHAPES = [(2, 2), (4, 2), (2, 16), (32, 4), (64, 4), (16, 16), (30, 6), (128, 2), (256, 4),
+          (6, 42), (512, 2)]
+PATHS = ["tma", "explicit"]
+
+
+@pytest.mark.parametrize("name", sorted({k.split("__")[0]
+                                          for k in np.load(GOLDEN).files}))
+@pytest.mark.parametrize("path", PATHS)
+def test_golden_cases(name, path):
+    z = np.load(GOLDEN)
+    x, y = z[f"{name}__in"], z[f"{name}__out"]
+    n, s, e, w, nearest, cx, ins = (int(v) for v in z[f"{name}__meta"])
+    st = Stencil(op=str(z[f"{name}__op"]), dtype=str(x.dtype), north=n, south=s, east=e, west=w,
+                 border="nearest" if nearest else "pad", pad_value=float(z[f"{name}__pad"][0]),
+                 complexity=cx, instructions=ins, load_path=path)
+    # x is 23x37: fp32 rows are 148 B (not 16-B aligned) -> pad the pitch for TMA.
+    for wc, wr in [(4, 2), (8, 8), (32, 4), (2, 30)]:
+        a = torch.zeros((x.shape[0], 40), dtype=TDT[str(x.dtype)], device="cuda")
+        a[:, :x.shape[1]] = to_dev(x)
+        b = torch.zeros_like(a)
+        st(a[:, :x.shape[1]], b[:, :x.shape[1]], wc, wr)
+        torch.cuda.synchronize()
+        got = b[:, :x.shape[1]].cpu().numpy()
+        assert_same(got, y, f"{name} {path} {wc}x{wr}")
+
+
+CASES = [
+    ("five_point", "float32", (1, 1, 1, 1), "pad", 0.0),
+    ("five_point", "float32", (1, 1, 1, 1), "pad", 1.0),
+    ("five_point", "float64", (1, 1, 1, 1), "nearest", 0.0),
+    ("heat", "float32", (1, 1, 1, 1), "nearest", 0.0),
+    ("gol", "int32", (1, 1, 1, 1), "pad", 0.0),
+    ("gol", "int32", (1, 1, 1, 1), "nearest", 0.0),
+    ("boxmean", "float32", (5, 1, 3, 0), "nearest", 0.0),
+    ("boxmean", "int32", (7, 2, 0, 9), "pad", -3.0),
+    ("gaussian", "float32", (5, 5, 5, 5), "nearest", 0.0),
+    ("gaussian", "int32", (10, 10, 10, 10), "pad", 0.0),
+    ("sobel", "float64", (1, 1, 1, 1), "nearest", 0.0),
+    ("nms", "float32", (1, 1, 1, 1), "pad", 0.0),
+    ("threshold", "int32", (0, 0, 0, 0), "pad", 0.0),
+]
+
+
+@pytest.mark.parametrize("op,dtype,borders,border,pad", CASES)
+@pytest.mark.parametrize("path", PATHS)
+def test_ops_vs_oracle_ragged(op, dtype, borders, border, pad, path):
+    n, s, e, w = borders
+    st = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w, border=border,
+                 pad_value=pad, load_path=path)
+    H, W = 203, 264  # ragged vs every block shape; W*4 B is 16-B aligned
+    x = rand_grid(dtype, (H, W), 11, op)
+    want = O.stencil(O.desc_from_stencil(st), x)
+    for wc, wr in SHAPES:
+        if wc + e + w > 256 and path == "tma":
+            continue
+        got = gpu_pass(st, x, wc, wr)
+        assert_same(got, want, f"{op}/{dtype}/{border} {path} {wc}x{wr}")
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64", "int32"])
+@pytest.mark.parametrize("cx,ins", [(0, 100), (1, 650)])
+def test_synthetic_vs_oracle(dtype, cx, ins):
+    st = Stencil(op="synthetic", dtype=dtype, north=17, south=3, east=30, west=1,
+                 border="nearest", complexity=cx, instructions=ins)
+    x = rand_grid(dtype, (97, 160), 5)
+    want = O.stencil(O.desc_from_stencil(st), x)
+    for wc, wr in [(32, 8), (2, 64), (96, 2), (16, 6)]:
+        assert_same(gpu_pass(st, x, wc, wr), want, f"synthetic {dtype} {wc}x{wr}")
+
+
+def test_gol_config2_bit_exact_iterated():
+    # BASELINE config 2 at a size the oracle finishes in seconds: 100 generations.
+    st = Stencil(op="gol", dtype="int32")
+    x = rand_grid("int32", (512, 512), 2, "gol")
+    want = O.iterate(O.desc_from_stencil(st), x, 100)
+    a, b = to_dev(x), torch.empty((512, 512), dtype=torch.int32, device="cuda")
+    res = st.iterate(a, b, 100, 32, 8)
+    torch.cuda.synchronize()
+    assert res.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_gol_full_size_properties():
+    # Full BASELINE config-2 size: 8192^2, 100 generations.  The CPU oracle is
+    # too slow here, so check size-independent properties: two block shapes
+    # and both load paths agree bit-for-bit, outputs are {0,1}, and a periodic
+    # tiling of blinkers is reproduced exactly.
+    n = 8192
+    x = rand_grid("int32", (n, n), 2, "gol")
+    outs = []
+    for wc, wr, path in [(32, 8, "tma"), (64, 4, "explicit"), (128, 2, "tma")]:
+        st = Stencil(op="gol", dtype="int32", load_path=path)
+        a, b = to_dev(x), torch.empty((n, n), dtype=torch.int32, device="cuda")
+        outs.append(st.iterate(a, b, 100, wc, wr).cpu().numpy())
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
+    assert set(np.unique(outs[0])) <= {0, 1}
+    # blinkers on a 5-periodic lattice away from the edges: period 2
+    g = np.zeros((n, n), np.int32)
+    g[8:n - 8:5, 9:n - 8:5] = 1
+    g[8:n - 8:5, 10:n - 7:5] = 1
+    g[8:n - 8:5, 11:n - 6:5] = 1
+    st = Stencil(op="gol", dtype="int32")
+    a, b = to_dev(g), torch.empty((n, n), dtype=torch.int32, device="cuda")
+    assert st.iterate(a, b, 100, 32, 8).cpu().numpy().tobytes() == g.tobytes()
+
+
+def test_heat_config3_subset_iterated():
+    st = Stencil(op="heat", dtype="float32", border="nearest")
+    x = rand_grid("float32", (300, 520), 3)
+    want = O.iterate(O.desc_from_stencil(st), x, 10)
+    a, b = to_dev(x), torch.empty_like(to_dev(x))
+    got = st.iterate(a, b, 10, 64, 4).cpu().numpy()
+    assert_same(got, want, "heat x10")
+
+
+def test_halo_rows_match_full_grid():
+    st = Stencil(op="boxmean", dtype="float32", north=3, south=2, east=1, west=2,
+                 border="nearest")
+    x = rand_grid("float32", (64, 96), 9)
+    full = gpu_pass(st, x, 32, 4)
+    for path in PATHS:
+        st2 = Stencil(op="boxmean", dtype="float32", north=3, south=2, east=1, west=2,
+                      border="nearest", load_path=path)
+        r0, r1 = 20, 41
+        shard = to_dev(x[r0 - 3:r1 + 2])
+        out = torch.empty((r1 - r0, 96), dtype=torch.float32, device="cuda")
+        st2(shard[3:], out, 16, 8, rows_above=3, rows_below=2, height=r1 - r0)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == full[r0:r1].tobytes()
+
+
+def test_oversized_and_refused():
+    st = Stencil(op="gol", dtype="int32")
+    a = torch.zeros((64, 64), dtype=torch.int32, device="cuda")
+    b = torch.zeros_like(a)
+    with pytest.raises(IllegalWorkgroupSize):
+        st(a, b, 64, 32)  # 2048 threads
+    assert st.probe(64, 64, 64, 32)["status"] == "OVERSIZED"
+    # border 64 in f64 with a 512x2 block: tile (512+128)x(2+128)x8 B > 227 KB
+    big = Stencil(op="boxmean", dtype="float64", north=64, south=64, east=64, west=64)
+    assert big.probe(4096, 4096, 512, 2)["status"] == "REFUSED"
+    a64 = torch.zeros((256, 1024), dtype=torch.float64, device="cuda")
+    with pytest.raises(RefusedParameter) as ei:
+        big(a64, torch.zeros_like(a64), 512, 2)
+    assert (ei.value.w_c, ei.value.w_r) == (512, 2)
+    # the context is still usable after a refusal
+    st(a, b, 32, 8)
+    torch.cuda.synchronize()
+
+
+def test_kernel_max_and_probe_fields():
+    st = Stencil(op="five_point", dtype="float32")
+    km = st.kernel_max()
+    assert 64 <= km <= 1024
+    p = st.probe(1024, 1024, 32, 8)
+    assert p["status"] == "OK" and p["load_path"] == "tma"
+    assert p["tile_bytes"] == (32 + 2) * (8 + 2) * 4
+
+
+def test_timing_returns_positive_samples():
+    st = Stencil(op="five_point", dtype="float32")
+    a = to_dev(rand_grid("float32", (1024, 1024), 1))
+    b = torch.empty_like(a)
+    ms = st.time(a, b, 32, 8, samples=5, warmup=2)
+    assert len(ms) == 5 and all(t > 0 for t in ms)
+
+
+def test_run_host_end_to_end():
+    st = Stencil(op="gol", dtype="int32")
+    x = rand_grid("int32", (256, 300), 4, "gol")
+    out = np.empty_like(x)
+    st.run_host(x, out, 7, 32, 4)
+    want = O.iterate(O.desc_from_stencil(st), x, 7)
+    assert out.tobytes() == want.tobytes()
