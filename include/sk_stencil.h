@@ -93,6 +93,10 @@ typedef struct {
   int32_t complexity;  /* synthetic only: 0 light (synthetic-a), 1 heavy (b) */
   int32_t instructions;/* synthetic only: static instruction total          */
   int32_t load_path;   /* sk_load_path                                      */
+  int32_t cells_per_thread; /* K cells per work-item (rows of one column):
+                          0 = auto, or 1, 2, 4, 8.  The workgroup (block) is
+                          still wc x wr work-items; its tile covers
+                          wc x (wr*K) cells.                                 */
 } sk_stencil_desc;
 
 /* Launch one stencil pass over a W x H region, out-of-place, on `stream`

@@ -1,0 +1,34 @@
+#!/usr/bin/env bash
+# Compiles the reference wgtune library (the tuner side of the path: space,
+# features, synthgen, simoracle, datastore, learn, tuner, bench) directly from
+# its sources under /root/reference — no CMake, no copies into this repo —
+# into oracle/_ref/ (git-ignored; travels to the GPU box as built files).
+# Used only by tests/ as the parity checker for the host C++ tuner.
+#
+# Third-party: nlohmann/json (unpinned by the reference, vendor/ is absent;
+# we use the 3.11.3 copy shipped in this image under cudnn_frontend).
+# serve.cpp (TCP daemon, out of scope) is excluded.
+set -euo pipefail
+REF=/root/reference/proj
+HERE="$(cd "$(dirname "$0")" && pwd)"
+OUT="$HERE/_ref"
+JSON_INC=/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
+CXX=${CXX:-g++}
+[ -d "$REF/src" ] || { echo "reference sources not present; skipping"; exit 0; }
+mkdir -p "$OUT/obj"
+SRCS="space scenario features synthgen simoracle datastore learn tuner bench"
+stamp="$OUT/libwgtune_ref.a"
+need=0
+for s in $SRCS; do
+  [ "$stamp" -nt "$REF/src/$s.cpp" ] || need=1
+done
+[ -f "$stamp" ] || need=1
+if [ "$need" = 1 ]; then
+  for s in $SRCS; do
+    $CXX -std=c++20 -O2 -fPIC -I"$REF/include" -I"$JSON_INC" -c "$REF/src/$s.cpp" -o "$OUT/obj/$s.o" &
+  done
+  wait
+  rm -f "$stamp"
+  ar rcs "$stamp" "$OUT"/obj/*.o
+fi
+echo "$OUT/libwgtune_ref.a"

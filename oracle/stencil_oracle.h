@@ -33,7 +33,8 @@ typedef struct {
   int32_t border_mode;
   double pad_value;
   int32_t complexity, instructions;
-  int32_t load_path; /* ignored */
+  int32_t load_path;        /* ignored */
+  int32_t cells_per_thread; /* ignored */
 } oracle_desc;
 
 /* One pass over a W x H region (row pitch in elements); rows_above /

@@ -55,6 +55,7 @@ class sk_stencil_desc(ctypes.Structure):
         ("complexity", ctypes.c_int32),
         ("instructions", ctypes.c_int32),
         ("load_path", ctypes.c_int32),
+        ("cells_per_thread", ctypes.c_int32),
     ]
 
 

@@ -32,10 +32,15 @@ struct Geom {
   long long pitch_out;      // elements
   int above, below;         // readable input rows beyond [0, H) (row-shard halos)
   int N, S, E, Wb;          // border region (Wb = west)
-  int wc, wr;               // workgroup (block) shape
+  int wc, wr;               // workgroup (block) shape, threads
+  int K;                    // cells per work-item (consecutive rows of one column)
+  int tile_rows;            // output rows per tile = wr * K
+  int ex_lo, ex_hi;         // tiles with ex_lo <= tx <= ex_hi and
+  int ey_lo, ey_hi;         //   ey_lo <= ty <= ey_hi need no border work
   int lw;                   // logical tile width  = wc + E + Wb
-  int tile_w;               // smem row pitch (lw padded to 16 B)
-  int tile_h;               // tile rows = wr + N + S
+  int tile_w;               // smem row pitch = TMA box width (16-B multiple)
+  int vec;                  // elements per 16 B (TMA: box x start must be 16-B aligned)
+  int tile_h;               // tile rows = tile_rows + N + S
   int tiles_x, tiles_y;
   int mode;                 // sk_border_mode
   int pad_is_zero;          // PAD mode with an all-zero pad value
@@ -58,6 +63,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
@@ -108,10 +117,17 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
 
-// True when a tile reaches outside the readable input (needs substitution).
-__device__ __forceinline__ bool tile_is_edge(const Geom& g, int r0, int c0) {
-  return (r0 - g.N < -g.above) || (r0 + g.wr + g.S > g.H + g.below) || (c0 - g.Wb < 0) ||
-         (c0 + g.wc + g.E > g.W);
+// Column offset of the tile's first logical cell inside its 16-B aligned
+// TMA box: the box starts at align_down(c0 - W, vec) (the TMA unit faults on
+// an unaligned innermost start coordinate).
+__device__ __forceinline__ int tile_offset(const Geom& g, int c0) {
+  return (c0 - g.Wb) & (g.vec - 1);
+}
+
+// True when a tile reaches outside the readable input or the matrix (needs
+// border substitution and bounds-checked stores); bounds precomputed on the host.
+__device__ __forceinline__ bool tile_is_edge(const Geom& g, int tx, int ty) {
+  return tx < g.ex_lo || tx > g.ex_hi || ty < g.ey_lo || ty > g.ey_hi;
 }
 
 // Patch the out-of-range cells of an edge tile in shared memory: pad value,
@@ -121,6 +137,7 @@ __device__ __forceinline__ bool tile_is_edge(const Geom& g, int r0, int c0) {
 template <typename T>
 __device__ __forceinline__ void fixup_tile(T* tile, const Geom& g, int r0, int c0, T pad,
                                            int tid, int nthreads) {
+  // `tile` points at the first logical column (box start + tile_offset).
   const int total = g.tile_h * g.lw;
   const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
   for (int i = tid; i < total; i += nthreads) {
@@ -142,78 +159,151 @@ __device__ __forceinline__ void fixup_tile(T* tile, const Geom& g, int r0, int c
   }
 }
 
+// ------------------------------------------------------- compute + store
+// Work-item (threadIdx.x, threadIdx.y) owns column c0 + threadIdx.x, rows
+// r0 + threadIdx.y*K ... + K-1 of the tile.  The K evaluations are unrolled
+// so the compiler shares the overlapping shared-memory loads between them.
+template <class Op, typename T, int K>
+__device__ __forceinline__ void compute_tile(const T* tile, const Geom& g,
+                                             const OpParams<T>& p, T (&res)[K]) {
+  const Op op;
+  const T* base = tile + (threadIdx.y * K + g.N) * g.tile_w + threadIdx.x + g.Wb;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    TileView<T> view{base + j * g.tile_w, g.tile_w};
+    res[j] = op.template apply<T>(view, p);
+  }
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void store_tile(T* __restrict__ out, const Geom& g, int r0, int c0,
+                                           bool edge, const T (&res)[K]) {
+  const int c = c0 + threadIdx.x;
+  const int r = r0 + threadIdx.y * K;
+  T* dst = out + static_cast<long long>(r) * g.pitch_out + c;
+  if (!edge) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) dst[j * g.pitch_out] = res[j];
+  } else if (c < g.W) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (r + j < g.H) dst[j * g.pitch_out] = res[j];
+    }
+  }
+}
+
 // --------------------------------------------------------------------- K1a
-template <class Op, typename T>
+template <typename T>
 __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage, uint64_t* bar,
                                                const Geom& g, int t) {
   int ty = t / g.tiles_x;
   int tx = t - ty * g.tiles_x;
   int x = tx * g.wc - g.Wb;
-  int y = ty * g.wr - g.N + g.above;  // tensor rows start `above` rows before row 0
+  x -= x & (g.vec - 1);                      // 16-B aligned innermost start
+  int y = ty * g.tile_rows - g.N + g.above;  // tensor rows start `above` rows before row 0
   mbar_arrive_expect_tx(bar, static_cast<uint32_t>(g.nchunks * g.box_h * g.tile_w * sizeof(T)));
   for (int k = 0; k < g.nchunks; ++k) {
     tma_load_2d(stage + k * g.box_h * g.tile_w, map, bar, x, y + k * g.box_h);
   }
 }
 
-template <class Op, typename T, int MAXT>
+template <class Op, typename T, int K, int MAXT>
 __global__ void __launch_bounds__(MAXT)
     k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
                   const T pad, const __grid_constant__ OpParams<T> p) {
+  // Shared memory: [stages x stage_bytes tiles][full[stages]][empty[stages]].
+  // full[s]  : 1 arrival (producer's expect_tx) + the TMA transaction bytes.
+  // empty[s] : one arrival per warp once it has read the tile in stage s.
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.stages * g.stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * g.stage_bytes);
+  uint64_t* empty = full + g.stages;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nthreads = blockDim.x * blockDim.y;
+  const int nwarps = (nthreads + 31) >> 5;
   const int ntiles = g.tiles_x * g.tiles_y;
   const bool fix_edges = !(g.mode == 0 && g.pad_is_zero);
+  // Refill lag: the stage read `lag` iterations ago is refilled, so the
+  // producer rarely waits for slow warps (lag 1 for shallow rings).
+  const int lag = g.stages >= 3 ? 2 : 1;
+  const int lane = tid & 31;
+  const int warp_lanes = min(32, nthreads - (tid & ~31));
+  const unsigned warp_mask = warp_lanes == 32 ? 0xffffffffu : ((1u << warp_lanes) - 1u);
 
   if (tid == 0) {
     prefetch_tensormap(&map);
-    for (int s = 0; s < g.stages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < g.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nwarps);
+    }
     fence_barrier_init();
     fence_proxy_async_smem();
     for (int s = 0; s < g.stages; ++s) {
       int t = blockIdx.x + s * gridDim.x;
       if (t < ntiles) {
-        tma_issue_tile<Op, T>(&map, reinterpret_cast<T*>(smem + s * g.stage_bytes), &bars[s], g,
-                              t);
+        tma_issue_tile<T>(&map, reinterpret_cast<T*>(smem + s * g.stage_bytes), &full[s], g, t);
       }
     }
   }
   __syncthreads();
 
-  const Op op;
-  int iter = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-    const int s = iter % g.stages;
-    const uint32_t parity = static_cast<uint32_t>((iter / g.stages) & 1);
-    T* tile = reinterpret_cast<T*>(smem + s * g.stage_bytes);
-    const int ty = t / g.tiles_x;
-    const int r0 = ty * g.wr;
-    const int c0 = (t - ty * g.tiles_x) * g.wc;
+  // Tile coordinates advance by gridDim.x tiles per iteration; kept
+  // incrementally (no per-tile integer division on the hot path).
+  const int step_y = gridDim.x / g.tiles_x;
+  const int step_x = gridDim.x - step_y * g.tiles_x;
+  int ty = blockIdx.x / g.tiles_x;
+  int tx = blockIdx.x - ty * g.tiles_x;
+  int s = 0;
+  uint32_t phase = 0;
+  int ps = 0;  // producer (thread 0): stage / phase of iteration it - lag
+  uint32_t pphase = 0;
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    if (tid == 0 && it >= lag) {
+      // refill the stage read at iteration it-lag with tile (it-lag)+stages
+      int tn = t + (g.stages - lag) * gridDim.x;
+      if (tn < ntiles) {
+        mbar_wait_parity(&empty[ps], pphase);
+        tma_issue_tile<T>(&map, reinterpret_cast<T*>(smem + ps * g.stage_bytes), &full[ps], g,
+                          tn);
+      }
+      if (++ps == g.stages) {
+        ps = 0;
+        pphase ^= 1u;
+      }
+    }
+    const int r0 = ty * g.tile_rows;
+    const int c0 = tx * g.wc;
+    const bool edge = tile_is_edge(g, tx, ty);
+    T* tile = reinterpret_cast<T*>(smem + s * g.stage_bytes) + tile_offset(g, c0);
 
-    mbar_wait_parity(&bars[s], parity);
-    if (fix_edges && tile_is_edge(g, r0, c0)) {
+    mbar_wait_parity(&full[s], phase);
+    if (fix_edges && edge) {
+      __syncthreads();  // every warp is at this tile (uniform condition)
       fixup_tile(tile, g, r0, c0, pad, tid, nthreads);
       fence_proxy_async_smem();  // generic writes before the next async refill
       __syncthreads();
     }
+    T res[K];
+    compute_tile<Op, T, K>(tile, g, p, res);
+    __syncwarp(warp_mask);
+    if (lane == 0) mbar_arrive(&empty[s]);
+    store_tile<T, K>(out, g, r0, c0, edge, res);
 
-    const int r = r0 + threadIdx.y;
-    const int c = c0 + threadIdx.x;
-    TileView<T> view{tile + (threadIdx.y + g.N) * g.tile_w + threadIdx.x + g.Wb, g.tile_w};
-    T res = op.template apply<T>(view, p);
-    __syncthreads();  // every work-item has read stage s
-    if (tid == 0) {
-      int tn = t + g.stages * gridDim.x;
-      if (tn < ntiles) tma_issue_tile<Op, T>(&map, tile, &bars[s], g, tn);
+    tx += step_x;
+    ty += step_y;
+    if (tx >= g.tiles_x) {
+      tx -= g.tiles_x;
+      ++ty;
     }
-    if (r < g.H && c < g.W) out[static_cast<long long>(r) * g.pitch_out + c] = res;
+    if (++s == g.stages) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
 }
 
 // --------------------------------------------------------------------- K1b
-template <class Op, typename T, int MAXT>
+template <class Op, typename T, int K, int MAXT>
 __global__ void __launch_bounds__(MAXT)
     k_stencil_explicit(const T* __restrict__ in, T* __restrict__ out, const Geom g, const T pad,
                        const __grid_constant__ OpParams<T> p) {
@@ -221,12 +311,15 @@ __global__ void __launch_bounds__(MAXT)
   T* tile = reinterpret_cast<T*>(smem);
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nthreads = blockDim.x * blockDim.y;
-  const int r0 = blockIdx.y * g.wr;
-  const int c0 = blockIdx.x * g.wc;
+  const int by = blockIdx.x / g.tiles_x;  // 1-D grid of tiles (no 65535 limit)
+  const int bx = blockIdx.x - by * g.tiles_x;
+  const int r0 = by * g.tile_rows;
+  const int c0 = bx * g.wc;
   const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
   const int total = g.tile_h * g.lw;
+  const bool edge = tile_is_edge(g, bx, by);
 
-  if (!tile_is_edge(g, r0, c0)) {
+  if (!edge) {
     for (int i = tid; i < total; i += nthreads) {
       int tr = i / g.lw;
       int tc = i - tr * g.lw;
@@ -252,14 +345,9 @@ __global__ void __launch_bounds__(MAXT)
     }
   }
   __syncthreads();
-
-  const int r = r0 + threadIdx.y;
-  const int c = c0 + threadIdx.x;
-  if (r < g.H && c < g.W) {
-    const Op op;
-    TileView<T> view{tile + (threadIdx.y + g.N) * g.tile_w + threadIdx.x + g.Wb, g.tile_w};
-    out[static_cast<long long>(r) * g.pitch_out + c] = op.template apply<T>(view, p);
-  }
+  T res[K];
+  compute_tile<Op, T, K>(tile, g, p, res);
+  store_tile<T, K>(out, g, r0, c0, edge, res);
 }
 
 }  // namespace sk

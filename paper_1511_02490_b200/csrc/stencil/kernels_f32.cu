@@ -1,0 +1,5 @@
+// Kernel instantiations for float.
+#include <cstdint>
+#define SK_T float
+#define SK_REGISTRY_FN kernels_f32
+#include "kernels_inst.cuh"

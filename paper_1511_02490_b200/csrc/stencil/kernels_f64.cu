@@ -1,0 +1,5 @@
+// Kernel instantiations for double.
+#include <cstdint>
+#define SK_T double
+#define SK_REGISTRY_FN kernels_f64
+#include "kernels_inst.cuh"

@@ -1,0 +1,5 @@
+// Kernel instantiations for int32_t.
+#include <cstdint>
+#define SK_T int32_t
+#define SK_REGISTRY_FN kernels_i32
+#include "kernels_inst.cuh"

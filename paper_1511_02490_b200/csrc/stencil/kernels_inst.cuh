@@ -1,0 +1,47 @@
+// Instantiates every (op, K) kernel pair for one element type SK_T and
+// defines the registry function SK_REGISTRY_FN (see registry.cuh).
+#include "kernels.cuh"
+#include "registry.cuh"
+
+namespace sk {
+namespace {
+
+template <class Op, typename T, int K>
+KernelPair pair_for() {
+  return {reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, K, 1024>),
+          reinterpret_cast<KernelPtr>(&k_stencil_explicit<Op, T, K, 1024>)};
+}
+
+template <class Op, typename T>
+KernelPair pair_for_k(int K) {
+  switch (K) {
+    case 1: return pair_for<Op, T, 1>();
+    case 2: return pair_for<Op, T, 2>();
+    case 4: return pair_for<Op, T, 4>();
+    default: return pair_for<Op, T, 8>();
+  }
+}
+
+}  // namespace
+
+KernelPair SK_REGISTRY_FN(const sk_stencil_desc& d, int K) {
+  using T = SK_T;
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return pair_for_k<FivePoint, T>(K);
+    case SK_OP_HEAT: return pair_for_k<Heat, T>(K);
+    case SK_OP_GOL: return pair_for_k<Gol, T>(K);
+    case SK_OP_BOXMEAN:
+      if (d.north == 5 && d.south == 1 && d.east == 3 && d.west == 0) {
+        return pair_for_k<BoxMeanFixed<5, 1, 3, 0>, T>(K);
+      }
+      return pair_for_k<BoxMean, T>(K);
+    case SK_OP_GAUSSIAN: return pair_for_k<Gaussian, T>(K);
+    case SK_OP_SOBEL: return pair_for_k<Sobel, T>(K);
+    case SK_OP_NMS: return pair_for_k<Nms, T>(K);
+    case SK_OP_THRESHOLD: return pair_for_k<Threshold, T>(K);
+    case SK_OP_SYNTHETIC: return pair_for_k<Synthetic, T>(K);
+  }
+  return {nullptr, nullptr};
+}
+
+}  // namespace sk

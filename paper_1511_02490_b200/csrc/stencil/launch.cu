@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "registry.cuh"
 #include "sk_stencil.h"
 
 namespace sk {
@@ -86,6 +87,22 @@ int current_device_info(DeviceInfo* out, int* dev_out = nullptr) {
   return SK_OK;
 }
 
+long long floor_div(long long a, long long b) {
+  long long q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+long long ceil_div(long long a, long long b) { return -floor_div(-a, b); }
+
+// Cells per work-item: the descriptor's value, or AUTO = the largest of
+// {8, 4, 2, 1} keeping the tile at most 64 output rows (and no taller than
+// the grid needs).
+int cells_per_thread(const sk_stencil_desc& d, int wr, long long H) {
+  if (d.cells_per_thread > 0) return d.cells_per_thread;
+  int k = 8;
+  while (k > 1 && (static_cast<long long>(wr) * k > 64 || static_cast<long long>(wr) * k > H)) k /= 2;
+  return k;
+}
+
 // ------------------------------------------------------------ op parameters
 long long binom(int n, int k) {
   long long r = 1;
@@ -136,6 +153,10 @@ int validate_desc(const sk_stencil_desc* d) {
   for (int b : {d->north, d->south, d->east, d->west}) {
     if (b < 0 || b > 64) return fail(SK_EINVAL, "border values must be in [0, 64]");
   }
+  if (d->cells_per_thread != 0 && d->cells_per_thread != 1 && d->cells_per_thread != 2 &&
+      d->cells_per_thread != 4 && d->cells_per_thread != 8) {
+    return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
+  }
   int need = 0;
   switch (d->op) {
     case SK_OP_FIVE_POINT: case SK_OP_HEAT: case SK_OP_GOL: case SK_OP_SOBEL: case SK_OP_NMS:
@@ -160,44 +181,11 @@ int validate_desc(const sk_stencil_desc* d) {
 }
 
 // --------------------------------------------------------- kernel registry
-using KernelPtr = const void*;
-
-struct KernelPair {
-  KernelPtr tma;
-  KernelPtr explicit_;
-};
-
-template <class Op, typename T>
-KernelPair kernels_for() {
-  return {reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1024>),
-          reinterpret_cast<KernelPtr>(&k_stencil_explicit<Op, T, 1024>)};
-}
-
-template <typename T>
-KernelPair kernels_for_op(const sk_stencil_desc& d) {
-  switch (d.op) {
-    case SK_OP_FIVE_POINT: return kernels_for<FivePoint, T>();
-    case SK_OP_HEAT: return kernels_for<Heat, T>();
-    case SK_OP_GOL: return kernels_for<Gol, T>();
-    case SK_OP_BOXMEAN:
-      if (d.north == 5 && d.south == 1 && d.east == 3 && d.west == 0) {
-        return kernels_for<BoxMeanFixed<5, 1, 3, 0>, T>();
-      }
-      return kernels_for<BoxMean, T>();
-    case SK_OP_GAUSSIAN: return kernels_for<Gaussian, T>();
-    case SK_OP_SOBEL: return kernels_for<Sobel, T>();
-    case SK_OP_NMS: return kernels_for<Nms, T>();
-    case SK_OP_THRESHOLD: return kernels_for<Threshold, T>();
-    case SK_OP_SYNTHETIC: return kernels_for<Synthetic, T>();
-  }
-  return {nullptr, nullptr};
-}
-
-KernelPair kernels_for_desc(const sk_stencil_desc& d) {
+KernelPair kernels_for_desc(const sk_stencil_desc& d, int K) {
   switch (d.dtype) {
-    case SK_INT32: return kernels_for_op<int32_t>(d);
-    case SK_FLOAT32: return kernels_for_op<float>(d);
-    default: return kernels_for_op<double>(d);
+    case SK_INT32: return kernels_i32(d, K);
+    case SK_FLOAT32: return kernels_f32(d, K);
+    default: return kernels_f64(d, K);
   }
 }
 
@@ -339,7 +327,8 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   DeviceInfo info;
   int dev = 0;
   if (int rc = current_device_info(&info, &dev)) return rc;
-  KernelPair kp = kernels_for_desc(d);
+  const int K = cells_per_thread(d, wr, H);
+  KernelPair kp = kernels_for_desc(d, K);
   KernelAttr a_tma, a_exp;
   if (int rc = kernel_attr(dev, kp.tma, info, &a_tma)) return rc;
   if (int rc = kernel_attr(dev, kp.explicit_, info, &a_exp)) return rc;
@@ -359,12 +348,23 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   g.Wb = d.west;
   g.wc = wc;
   g.wr = wr;
+  g.K = K;
+  g.tile_rows = wr * K;
   g.lw = wc + d.east + d.west;
   const int vec = static_cast<int>(16 / es);
-  g.tile_w = (g.lw + vec - 1) / vec * vec;
-  g.tile_h = wr + d.north + d.south;
+  g.vec = vec;
+  // Box width: the logical tile plus the largest 16-B alignment offset any
+  // tile can have (constant when wc is a multiple of vec).
+  const int max_off = (wc % vec == 0) ? ((-d.west) & (vec - 1)) : vec - 1;
+  g.tile_w = (g.lw + max_off + vec - 1) / vec * vec;
+  g.tile_h = g.tile_rows + d.north + d.south;
   g.tiles_x = static_cast<int>((W + wc - 1) / wc);
-  g.tiles_y = static_cast<int>((H + wr - 1) / wr);
+  g.tiles_y = static_cast<int>((H + g.tile_rows - 1) / g.tile_rows);
+  // Interior tiles: read only inside the readable window and store in range.
+  g.ex_lo = static_cast<int>(ceil_div(d.west, wc));
+  g.ex_hi = static_cast<int>(floor_div(W - wc - d.east, wc));
+  g.ey_lo = static_cast<int>(ceil_div(std::max<long long>(0, d.north - g.above), g.tile_rows));
+  g.ey_hi = static_cast<int>(floor_div(H + g.below - d.south - g.tile_rows, g.tile_rows));
   g.mode = d.border_mode;
   g.pad_is_zero = d.pad_value == 0.0 && !std::signbit(d.pad_value);
   plan->tile_bytes = static_cast<long long>(g.lw) * g.tile_h * static_cast<long long>(es);
@@ -400,29 +400,32 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
     if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
       return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
     }
-    plan->grid = 0;  // 2-D grid (tiles_x, tiles_y)
+    plan->grid = g.tiles_x * g.tiles_y;  // one block per tile
     return SK_OK;
   }
 
+  // Boxes of <= 256 rows; a multiple of 8 rows keeps every box's shared
+  // destination 128-B aligned (tile_w * es is a 16-B multiple).
   g.nchunks = (g.tile_h + 255) / 256;
   g.box_h = (g.tile_h + g.nchunks - 1) / g.nchunks;
+  if (g.nchunks > 1) g.box_h = (g.box_h + 7) / 8 * 8;
   long long stage = static_cast<long long>(g.tile_w) * g.box_h * g.nchunks *
                     static_cast<long long>(es);
   stage = (stage + 127) / 128 * 128;
-  if (stage + 64 > attr.max_dyn_smem) {
+  if (stage + 128 > attr.max_dyn_smem) {
     return fail(SK_REFUSED, "tile %lld B exceeds shared memory %d B", stage, attr.max_dyn_smem);
   }
   g.stage_bytes = static_cast<int>(stage);
   // Ring depth: as deep as the per-block share of the SM's shared memory
   // allows at the thread-limited occupancy, between 2 and 8 stages.
   int occ2 = occupancy(dev, plan->kernel, plan->threads,
-                       static_cast<int>(std::min<long long>(2 * stage + 64, attr.max_dyn_smem)));
+                       static_cast<int>(std::min<long long>(2 * stage + 128, attr.max_dyn_smem)));
   int blocks = std::max(1, occ2);
-  long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 64;
+  long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 128;
   int stages = static_cast<int>(std::clamp<long long>(share / stage, 1, 8));
-  while (stages > 1 && stage * stages + 64 > attr.max_dyn_smem) --stages;
+  while (stages > 1 && stage * stages + 128 > attr.max_dyn_smem) --stages;
   g.stages = stages;
-  plan->smem = static_cast<int>(stage * stages + 64);
+  plan->smem = static_cast<int>(stage * stages + 16 * stages);  // + full/empty barriers
   int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem);
   if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
   long long ntiles = static_cast<long long>(g.tiles_x) * g.tiles_y;
@@ -458,7 +461,7 @@ int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, voi
     const T* tin = static_cast<const T*>(in);
     T* tout = static_cast<T*>(out);
     void* args[] = {&tin, &tout, const_cast<Geom*>(&plan.g), &pad, &p};
-    e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x, plan.g.tiles_y), block, args,
+    e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args,
                          plan.smem, stream);
   }
   if (e != cudaSuccess) {

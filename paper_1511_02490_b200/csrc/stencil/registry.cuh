@@ -1,0 +1,22 @@
+// Kernel registry: (op, dtype, K) -> {TMA kernel, explicit kernel}.  The
+// template instantiations live in one translation unit per element type
+// (kernels_i32.cu, kernels_f32.cu, kernels_f64.cu) so they build in parallel.
+#pragma once
+
+#include "sk_stencil.h"
+
+namespace sk {
+
+using KernelPtr = const void*;
+
+struct KernelPair {
+  KernelPtr tma;
+  KernelPtr explicit_;
+};
+
+// K in {1, 2, 4, 8}: cells per work-item.
+KernelPair kernels_i32(const sk_stencil_desc& d, int K);
+KernelPair kernels_f32(const sk_stencil_desc& d, int K);
+KernelPair kernels_f64(const sk_stencil_desc& d, int K);
+
+}  // namespace sk

@@ -63,6 +63,7 @@ class Stencil:
     complexity: int = 0          # synthetic kernels only
     instructions: int = 100      # synthetic kernels only
     load_path: str = "auto"      # "auto" | "tma" | "explicit"
+    cells_per_thread: int = 0    # K cells per work-item; 0 = auto
     _desc: N.sk_stencil_desc = field(init=False, repr=False)
 
     def __post_init__(self):
@@ -75,7 +76,8 @@ class Stencil:
             pad_value=float(self.pad_value), complexity=int(self.complexity),
             instructions=int(self.instructions),
             load_path={"auto": N.SK_LOAD_AUTO, "tma": N.SK_LOAD_TMA,
-                       "explicit": N.SK_LOAD_EXPLICIT}[self.load_path])
+                       "explicit": N.SK_LOAD_EXPLICIT}[self.load_path],
+            cells_per_thread=int(self.cells_per_thread))
 
     # -- construction from reference descriptors ---------------------------
     @classmethod

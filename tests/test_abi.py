@@ -22,7 +22,7 @@ def test_prototypes_cover_header():
 
 
 def test_descriptor_layout_matches_header():
-    # int32 x7, double, int32 x3 with natural alignment -> 56 bytes
+    # int32 x7 (+4 pad), double at 32, int32 x4 -> 56 bytes
     assert ctypes.sizeof(N.sk_stencil_desc) == 56
     assert N.sk_stencil_desc.pad_value.offset == 32
 
