@@ -32,3 +32,16 @@ if [ "$need" = 1 ]; then
   ar rcs "$stamp" "$OUT"/obj/*.o
 fi
 echo "$OUT/libwgtune_ref.a"
+
+# Tuner-side parity harness (tests/parity/tuner_parity.cpp): links the
+# reference library and the framework's libwgtb side by side.
+REPO="$(cd "$HERE/.." && pwd)"
+LIBDIR="$REPO/paper_1511_02490_b200/lib"
+HARNESS="$OUT/tuner_parity"
+if [ -f "$LIBDIR/libwgtb.so" ] && { [ ! -f "$HARNESS" ] || [ "$REPO/tests/parity/tuner_parity.cpp" -nt "$HARNESS" ] || [ "$LIBDIR/libwgtb.so" -nt "$HARNESS" ] || [ "$stamp" -nt "$HARNESS" ]; }; then
+  $CXX -std=c++20 -O2 -I"$REF/include" -I"$REPO/include" -I"$JSON_INC" -I/usr/local/cuda/include \
+    "$REPO/tests/parity/tuner_parity.cpp" -o "$HARNESS" "$stamp" \
+    -L"$LIBDIR" -lwgtb -lsk_stencil -L/usr/local/cuda/lib64 -lcudart -pthread \
+    -Wl,-rpath,"$LIBDIR" -Wl,-rpath,/usr/local/cuda/lib64
+fi
+echo "$HARNESS"
