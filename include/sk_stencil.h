@@ -150,7 +150,7 @@ int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_o
  * the reference (scenario.hpp:31-44) read from cudaDeviceProp instead of the
  * OpenCL device API. */
 typedef struct {
-  char name[128];          /* prop.name + PCI bus id, no '/', ',' or '\n'  */
+  char name[128];          /* prop.name, sanitised (no ' ', '/', ',', '\n') */
   int32_t compute_units;   /* multiProcessorCount                          */
   int32_t frequency_mhz;   /* cudaDevAttrClockRate / 1000                  */
   int32_t local_mem_kb;    /* sharedMemPerBlockOptin / 1024                */
@@ -171,6 +171,11 @@ int sk_device_features(int32_t device, sk_device_props* out);
  * uniform01() < 0.5 ? 1 : 0 (kind 2) or floor(256*uniform01()) (kind 3).
  * Generated on the host and copied. */
 int sk_fill_host(int32_t dtype, int32_t kind, uint64_t seed, void* h_out, int64_t count);
+
+/* Device-side bitwise comparison of two buffers (16-B aligned, size a
+ * multiple of 16): *equal = 1 when identical.  Used by the sweep's
+ * gold-standard check of every workgroup size. */
+int sk_buffers_equal(const void* d_a, const void* d_b, int64_t bytes, int32_t* equal);
 
 /* Last error text for the calling thread ("" if none). */
 const char* sk_last_error(void);

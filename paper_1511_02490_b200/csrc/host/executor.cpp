@@ -5,7 +5,6 @@
 
 #include <cuda_runtime.h>
 
-#include <cstring>
 #include <memory>
 #include <mutex>
 
@@ -156,7 +155,7 @@ CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig&
     Grids g(s, cfg);
     const auto space = enumerate_space(effective_max(s, cfg));
     std::set<WorkgroupSize>& refused = res.refused[s.id];
-    std::vector<unsigned char> gold, got;
+    void* gold = nullptr;  // output of the first measured size = the gold standard
     std::size_t mismatches = 0, done = 0;
     for (const WorkgroupSize& w : space) {
       const int rc = sk_stencil_probe(&d, s.dataset.width, s.dataset.height, w.cols(), w.rows(), nullptr,
@@ -173,14 +172,21 @@ CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig&
           continue;
         }
         if (cfg.validate) {
-          std::vector<unsigned char>& dst = gold.empty() ? gold : got;
-          dst.resize(g.bytes);
-          check_cuda(cudaMemcpy(dst.data(), g.out, g.bytes, cudaMemcpyDeviceToHost), "cudaMemcpy(out)");
-          if (&dst == &got && std::memcmp(gold.data(), got.data(), g.bytes) != 0) ++mismatches;
+          if (!gold) {
+            check_cuda(cudaMalloc(&gold, g.bytes), "cudaMalloc(gold)");
+            check_cuda(cudaMemcpy(gold, g.out, g.bytes, cudaMemcpyDeviceToDevice), "cudaMemcpy(gold)");
+          } else {
+            int32_t equal = 0;
+            if (sk_buffers_equal(gold, g.out, static_cast<int64_t>(g.bytes), &equal) != SK_OK) {
+              device_fail("sk_buffers_equal");
+            }
+            mismatches += equal ? 0 : 1;
+          }
         }
       }
       if (progress) progress(s, ++done, space.size());
     }
+    cudaFree(gold);
     res.gold_mismatches[s.id] = mismatches;
     res.contexts.emplace(s.id, scenario_context(s, cfg, refused));
   }

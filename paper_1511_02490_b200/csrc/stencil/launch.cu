@@ -504,6 +504,8 @@ struct Scratch {
   void* dev_a = nullptr;
   void* dev_b = nullptr;
   size_t dev_bytes = 0;
+  void* diff = nullptr;
+  std::vector<cudaEvent_t> events;
 };
 std::map<int, Scratch> g_scratch;
 
@@ -525,6 +527,18 @@ int scratch(Scratch** out) {
   }
   *out = &s;
   return SK_OK;
+}
+
+// Word-wise device comparison; *diff counts differing 16-B words.
+__global__ void k_count_diff(const uint4* __restrict__ a, const uint4* __restrict__ b, long long n,
+                             unsigned long long* diff) {
+  unsigned long long local = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint4 x = a[i], y = b[i];
+    local += (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+  }
+  if (local) atomicAdd(diff, local);
 }
 
 }  // namespace
@@ -610,21 +624,31 @@ int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, 
       return rc;
     }
   }
+  // All samples are enqueued back to back (flush, event, pass, event) and
+  // synchronised once; each sample is its own event pair on the stream.
+  if (static_cast<int>(s->events.size()) < 2 * samples) {
+    for (int i = static_cast<int>(s->events.size()); i < 2 * samples; ++i) {
+      cudaEvent_t ev;
+      if (cudaEventCreate(&ev) != cudaSuccess) return fail(SK_ECUDA, "cudaEventCreate failed");
+      s->events.push_back(ev);
+    }
+  }
   for (int i = 0; i < samples; ++i) {
     if (flush_l2) cudaMemsetAsync(s->flush, i & 0xff, s->flush_bytes, s->stream);
-    cudaEventRecord(s->ev0, s->stream);
+    cudaEventRecord(s->events[2 * i], s->stream);
     if (int rc = launch(*desc, d_in, d_out, width, height, pitch, pitch, 0, 0, wc, wr, s->stream)) {
+      cudaStreamSynchronize(s->stream);
       return rc;
     }
-    cudaEventRecord(s->ev1, s->stream);
-    cudaError_t e = cudaEventSynchronize(s->ev1);
-    if (e != cudaSuccess) return fail(SK_ECUDA, "sample failed: %s", cudaGetErrorString(e));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
-    ms_out[i] = ms;
+    cudaEventRecord(s->events[2 * i + 1], s->stream);
   }
   cudaError_t e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return fail(SK_ECUDA, "timing stream failed: %s", cudaGetErrorString(e));
+  for (int i = 0; i < samples; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]);
+    ms_out[i] = ms;
+  }
   return SK_OK;
 }
 
@@ -667,7 +691,9 @@ int sk_device_features(int32_t device, sk_device_props* out) {
   cudaError_t e = cudaGetDeviceProperties(&p, device);
   if (e != cudaSuccess) return fail(SK_ECUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
   std::memset(out, 0, sizeof(*out));
-  std::string name = std::string(p.name) + "-" + std::to_string(p.pciBusID);
+  // Stable across boxes (scenario ids embed it): the marketing name only;
+  // identical GPUs are the same tuning device.
+  std::string name = std::string(p.name);
   for (char& ch : name) {
     if (ch == '/' || ch == ',' || ch == '\n' || ch == ' ') ch = '-';
   }
@@ -686,6 +712,35 @@ int sk_device_features(int32_t device, sk_device_props* out) {
   out->cc_minor = p.minor;
   out->mem_clock_mhz = mem_khz / 1000;
   out->mem_bus_width = p.memoryBusWidth;
+  return SK_OK;
+}
+
+int sk_buffers_equal(const void* d_a, const void* d_b, int64_t bytes, int32_t* equal) {
+  g_last_error.clear();
+  if (!d_a || !d_b || !equal || bytes < 0) return fail(SK_EINVAL, "bad compare arguments");
+  if (bytes % 16 != 0 || reinterpret_cast<uintptr_t>(d_a) % 16 || reinterpret_cast<uintptr_t>(d_b) % 16) {
+    return fail(SK_EINVAL, "compare needs 16-B aligned buffers and sizes");
+  }
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  if (!s->diff && cudaMalloc(&s->diff, sizeof(unsigned long long)) != cudaSuccess) {
+    return fail(SK_ECUDA, "cudaMalloc(diff)");
+  }
+  cudaMemsetAsync(s->diff, 0, sizeof(unsigned long long), s->stream);
+  const long long words = bytes / 16;
+  DeviceInfo info;
+  current_device_info(&info);
+  const int grid = static_cast<int>(std::min<long long>((words + 255) / 256, 4LL * info.sms));
+  if (grid > 0) {
+    k_count_diff<<<grid, 256, 0, s->stream>>>(static_cast<const uint4*>(d_a),
+                                              static_cast<const uint4*>(d_b), words,
+                                              static_cast<unsigned long long*>(s->diff));
+  }
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, s->diff, sizeof h, cudaMemcpyDeviceToHost, s->stream);
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "compare failed: %s", cudaGetErrorString(e));
+  *equal = h == 0;
   return SK_OK;
 }
 

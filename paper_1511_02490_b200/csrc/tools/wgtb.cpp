@@ -5,7 +5,7 @@
 //                  [--device cuda|fixture] [--datasets standard|SIDExSIDE,...]
 //   wgtb collect   --scenarios DIR --out samples.csv [--refused F] [--contexts F]
 //                  [--samples 30] [--warmup 3] [--no-flush] [--no-validate] [--cap M]
-//                  [--border nearest|pad] [--k K] [--resume] [filters]
+//                  [--border nearest|pad] [--k K] [--store all|mean] [--resume] [filters]
 //   wgtb evaluate  --scenarios DIR --samples F --refused F --contexts F
 //                  --technique T|all --partition kfold|synthreal|loo-kernel|loo-dataset|loo-device
 //                  [--folds 10] [--seed S] [--metrics out.csv] [--pin-baseline WxH] [--expert]
@@ -15,6 +15,7 @@
 //   wgtb features  [--device 0]                 (cudaDeviceProp -> DeviceDescriptor JSON)
 //
 // Exit codes: 0 success, 1 internal error, 2 usage / input error.
+#include <chrono>
 #include <cstdio>
 #include <fstream>
 #include <iostream>
@@ -152,10 +153,20 @@ int cmd_collect(const Args& a) {
   std::size_t mismatches = 0;
   for (const Scenario& s : scenarios) {
     if (contexts.contains(s.id)) continue;
-    CollectResult r = collect({s}, cfg, [](const Scenario& sc, std::size_t done, std::size_t total) {
-      if (done == total) std::cerr << "  " << sc.id << ": " << total << " sizes\n";
+    const auto t0 = std::chrono::steady_clock::now();
+    CollectResult r = collect({s}, cfg, [&](const Scenario& sc, std::size_t done, std::size_t total) {
+      if (done == total) {
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::cerr << "  " << sc.id << ": " << total << " sizes in " << secs << " s\n";
+      }
     });
-    for (const auto& [w, runs] : r.table.scenario_rows(s.id)) table.add_row(s.id, w, runs);
+    // --store mean: one observation per test case, the sample mean (the
+    // evaluation only ever uses means; keeps full sweeps small on disk)
+    const bool mean_only = a.get("--store", "all") == "mean";
+    for (const auto& [w, runs] : r.table.scenario_rows(s.id)) {
+      if (mean_only) table.add_row(s.id, w, {r.table.mean_runtime(s.id, w)});
+      else table.add_row(s.id, w, runs);
+    }
     refused[s.id] = r.refused[s.id];
     contexts.emplace(s.id, r.contexts.at(s.id));
     mismatches += r.gold_mismatches[s.id];
