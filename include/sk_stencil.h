@@ -110,6 +110,22 @@ int sk_stencil_launch(const sk_stencil_desc* desc, const void* d_in, void* d_out
                       int64_t rows_above, int64_t rows_below, int32_t wc, int32_t wr,
                       void* stream);
 
+/* User customising functions: a C++/CUDA caller compiles
+ * the executor's kernel templates for its own functor (include/wgtb/
+ * stencil_custom.cuh) and passes the resulting kernel handles here; geometry,
+ * TMA descriptors, refusals and the launch are the library's.  Index [i] is
+ * K = 1, 2, 4, 8 cells per work-item.  desc->op is ignored (the functor is
+ * the op); borders, dtype, border mode and K are honoured. */
+typedef struct {
+  const void* tma[4];            /* k_stencil_tma<F, T, K, 1024>       */
+  const void* explicit_load[4];  /* k_stencil_explicit<F, T, K, 1024>  */
+} sk_kernel_table;
+
+int sk_stencil_launch_custom(const sk_stencil_desc* desc, const sk_kernel_table* kernels,
+                             const void* d_in, void* d_out, int64_t width, int64_t height,
+                             int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
+                             int64_t rows_below, int32_t wc, int32_t wr, void* stream);
+
 /* Iterated stencil: `iterations` passes ping-ponging between d_a (input) and
  * d_b.  The result lands in d_a when iterations is even, in d_b when odd;
  * *result_in_b (optional) says which.  Same pitch for both buffers. */

@@ -91,6 +91,8 @@ _desc_p = ctypes.POINTER(sk_stencil_desc)
 
 _PROTOTYPES = {
     "sk_stencil_launch": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp]),
+    "sk_stencil_launch_custom": (_i32, [_desc_p, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                                        _i32, _i32, _vp]),
     "sk_stencil_iterate": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp,
                                   ctypes.POINTER(_i32)]),
     "sk_stencil_probe": (_i32, [_desc_p, _i64, _i64, _i32, _i32, ctypes.POINTER(_i32),

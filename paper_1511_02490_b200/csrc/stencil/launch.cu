@@ -189,6 +189,37 @@ KernelPair kernels_for_desc(const sk_stencil_desc& d, int K) {
   }
 }
 
+// ------------------------------------------------ driver API (custom kernels)
+// Custom-functor kernels are registered in the CALLER's CUDA runtime, so they
+// arrive as driver CUfunction handles and are queried/launched with the
+// driver API (process-wide, context-shared).
+struct DriverApi {
+  CUresult (*func_get_attribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*func_set_attribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                     unsigned, CUstream, void**, void**) = nullptr;
+  bool ok = false;
+};
+
+const DriverApi& driver() {
+  static DriverApi api = [] {
+    DriverApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess;
+    };
+    a.ok = get("cuFuncGetAttribute", reinterpret_cast<void**>(&a.func_get_attribute)) &&
+           get("cuFuncSetAttribute", reinterpret_cast<void**>(&a.func_set_attribute)) &&
+           get("cuOccupancyMaxActiveBlocksPerMultiprocessor", reinterpret_cast<void**>(&a.occupancy)) &&
+           get("cuLaunchKernel", reinterpret_cast<void**>(&a.launch));
+    cudaGetLastError();
+    return a;
+  }();
+  return api;
+}
+
 // Per-(device, kernel) attributes: kernel max threads and the opt-in smem
 // attribute, set once.
 struct KernelAttr {
@@ -197,10 +228,31 @@ struct KernelAttr {
 };
 std::map<std::pair<int, KernelPtr>, KernelAttr> g_kattr;
 
-int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out) {
+
+
+int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out,
+                bool is_driver = false) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_pair(dev, k);
   auto it = g_kattr.find(key);
+  if (it == g_kattr.end() && is_driver) {
+    const DriverApi& api = driver();
+    if (!api.ok) return fail(SK_ECUDA, "driver entry points unavailable");
+    CUfunction f = reinterpret_cast<CUfunction>(const_cast<void*>(k));
+    int max_threads = 0, static_smem = 0;
+    if (api.func_get_attribute(&max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, f) != CUDA_SUCCESS ||
+        api.func_get_attribute(&static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, f) != CUDA_SUCCESS) {
+      return fail(SK_EINVAL, "custom kernel handle is not a valid CUfunction");
+    }
+    KernelAttr a;
+    a.max_threads = max_threads;
+    a.max_dyn_smem = info.smem_optin - static_smem;
+    if (api.func_set_attribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, a.max_dyn_smem) !=
+        CUDA_SUCCESS) {
+      return fail(SK_ECUDA, "cuFuncSetAttribute failed on custom kernel");
+    }
+    it = g_kattr.emplace(key, a).first;
+  }
   if (it == g_kattr.end()) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k);
@@ -222,14 +274,17 @@ int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out) {
 
 std::map<std::tuple<int, KernelPtr, int, int>, int> g_occ;
 
-int occupancy(int dev, KernelPtr k, int threads, int smem) {
+int occupancy(int dev, KernelPtr k, int threads, int smem, bool is_driver = false) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_occ.find({dev, k, threads, smem});
     if (it != g_occ.end()) return it->second;
   }
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) {
+  if (is_driver) {
+    CUfunction f = reinterpret_cast<CUfunction>(const_cast<void*>(k));
+    if (!driver().ok || driver().occupancy(&n, f, threads, static_cast<size_t>(smem)) != CUDA_SUCCESS) n = 0;
+  } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -306,6 +361,7 @@ int tensor_map(const MapKey& key, CUtensorMap* out) {
 struct Plan {
   Geom g{};
   KernelPtr kernel = nullptr;
+  bool driver_handle = false;  // kernel is a CUfunction of a custom functor
   bool tma = false;
   int threads = 0;
   int smem = 0;
@@ -316,9 +372,11 @@ struct Plan {
 
 // Builds the launch plan; returns SK_OK, SK_OVERSIZED, SK_REFUSED or an error.
 // `in` may be null for a probe (TMA eligibility then assumes aligned buffers).
+int k_index(int K) { return K == 1 ? 0 : K == 2 ? 1 : K == 4 ? 2 : 3; }
+
 int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
               long long pitch_out, long long above, long long below, int wc, int wr,
-              const void* in, Plan* plan) {
+              const void* in, Plan* plan, const sk_kernel_table* custom = nullptr) {
   if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) {
     return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
   }
@@ -328,10 +386,14 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   int dev = 0;
   if (int rc = current_device_info(&info, &dev)) return rc;
   const int K = cells_per_thread(d, wr, H);
-  KernelPair kp = kernels_for_desc(d, K);
+  KernelPair kp = custom ? KernelPair{custom->tma[k_index(K)], custom->explicit_load[k_index(K)]}
+                         : kernels_for_desc(d, K);
+  if (!kp.tma || !kp.explicit_) return fail(SK_EINVAL, "kernel table has no entry for K=%d", K);
+  const bool drv = custom != nullptr;
+  plan->driver_handle = drv;
   KernelAttr a_tma, a_exp;
-  if (int rc = kernel_attr(dev, kp.tma, info, &a_tma)) return rc;
-  if (int rc = kernel_attr(dev, kp.explicit_, info, &a_exp)) return rc;
+  if (int rc = kernel_attr(dev, kp.tma, info, &a_tma, drv)) return rc;
+  if (int rc = kernel_attr(dev, kp.explicit_, info, &a_exp, drv)) return rc;
 
   const long long threads = static_cast<long long>(wc) * wr;
   const size_t es = dtype_size(d.dtype);
@@ -397,7 +459,7 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
     g.box_h = g.tile_h;
     g.nchunks = 1;
     plan->smem = static_cast<int>(smem);
-    if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
+    if (occupancy(dev, plan->kernel, plan->threads, plan->smem, drv) < 1) {
       return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
     }
     plan->grid = g.tiles_x * g.tiles_y;  // one block per tile
@@ -419,18 +481,30 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   // Ring depth: as deep as the per-block share of the SM's shared memory
   // allows at the thread-limited occupancy, between 2 and 8 stages.
   int occ2 = occupancy(dev, plan->kernel, plan->threads,
-                       static_cast<int>(std::min<long long>(2 * stage + 128, attr.max_dyn_smem)));
+                       static_cast<int>(std::min<long long>(2 * stage + 128, attr.max_dyn_smem)), drv);
   int blocks = std::max(1, occ2);
   long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 128;
   int stages = static_cast<int>(std::clamp<long long>(share / stage, 1, 8));
   while (stages > 1 && stage * stages + 128 > attr.max_dyn_smem) --stages;
   g.stages = stages;
   plan->smem = static_cast<int>(stage * stages + 16 * stages);  // + full/empty barriers
-  int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem);
+  int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem, drv);
   if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
   long long ntiles = static_cast<long long>(g.tiles_x) * g.tiles_y;
   plan->grid = static_cast<int>(std::min<long long>(ntiles, static_cast<long long>(occ) * info.sms));
   return SK_OK;
+}
+
+int launch_driver(const Plan& plan, dim3 grid, dim3 block, void** args, cudaStream_t stream) {
+  CUfunction f = reinterpret_cast<CUfunction>(const_cast<void*>(plan.kernel));
+  CUresult r = driver().launch(f, grid.x, grid.y, grid.z, block.x, block.y, block.z,
+                               static_cast<unsigned>(plan.smem), reinterpret_cast<CUstream>(stream), args,
+                               nullptr);
+  if (r == CUDA_SUCCESS) return SK_OK;
+  if (r == CUDA_ERROR_INVALID_VALUE || r == CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES) {
+    return fail(SK_REFUSED, "launch refused (driver error %d)", static_cast<int>(r));
+  }
+  return fail(SK_ECUDA, "custom kernel launch failed (driver error %d)", static_cast<int>(r));
 }
 
 template <typename T>
@@ -456,11 +530,15 @@ int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, voi
     CUtensorMap map;
     if (int rc = tensor_map(key, &map)) return rc;
     void* args[] = {&map, &out, const_cast<Geom*>(&plan.g), &pad, &p};
+    if (plan.driver_handle) return launch_driver(plan, dim3(plan.grid), block, args, stream);
     e = cudaLaunchKernel(plan.kernel, dim3(plan.grid), block, args, plan.smem, stream);
   } else {
     const T* tin = static_cast<const T*>(in);
     T* tout = static_cast<T*>(out);
     void* args[] = {&tin, &tout, const_cast<Geom*>(&plan.g), &pad, &p};
+    if (plan.driver_handle) {
+      return launch_driver(plan, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args, stream);
+    }
     e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args,
                          plan.smem, stream);
   }
@@ -476,9 +554,9 @@ int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, voi
 
 int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
            long long pitch_in, long long pitch_out, long long above, long long below, int wc,
-           int wr, cudaStream_t stream) {
+           int wr, cudaStream_t stream, const sk_kernel_table* custom = nullptr) {
   Plan plan;
-  if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan)) {
+  if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan, custom)) {
     return rc;
   }
   long long used_above = plan.g.above;
@@ -562,6 +640,23 @@ int sk_stencil_launch(const sk_stencil_desc* desc, const void* d_in, void* d_out
   if (rows_above < 0 || rows_below < 0) return fail(SK_EINVAL, "negative halo rows");
   return launch(*desc, d_in, d_out, width, height, pitch_in, pitch_out, rows_above, rows_below,
                 wc, wr, static_cast<cudaStream_t>(stream));
+}
+
+int sk_stencil_launch_custom(const sk_stencil_desc* desc, const sk_kernel_table* kernels,
+                             const void* d_in, void* d_out, int64_t width, int64_t height,
+                             int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
+                             int64_t rows_below, int32_t wc, int32_t wr, void* stream) {
+  g_last_error.clear();
+  if (!kernels) return fail(SK_EINVAL, "null kernel table");
+  if (!desc) return fail(SK_EINVAL, "null descriptor");
+  sk_stencil_desc d = *desc;
+  d.op = SK_OP_BOXMEAN;  // the functor is the op; no op-specific border rule
+  if (int rc = validate_desc(&d)) return rc;
+  desc = &d;
+  if (!d_in || !d_out) return fail(SK_EINVAL, "null buffer");
+  if (rows_above < 0 || rows_below < 0) return fail(SK_EINVAL, "negative halo rows");
+  return launch(*desc, d_in, d_out, width, height, pitch_in, pitch_out, rows_above, rows_below,
+                wc, wr, static_cast<cudaStream_t>(stream), kernels);
 }
 
 int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
