@@ -110,6 +110,24 @@ def traffic_for(config: str, block: str):
 
 
 # --------------------------------------------------------------------- ours
+def predict_block(config: str, W: int, H: int, dtype: str):
+    """The autotuner's prediction (wgtb predict: trained model + live device
+    probe) for this scenario, or None when no trained bundle is present."""
+    model = ROOT / "results" / "b200" / "model.json"
+    kernel = ROOT / "results" / "b200" / "descriptors" / "kernels" / f"{'he' if config == 'heat' else config}.json"
+    wgtb = ROOT / "paper_1511_02490_b200" / "lib" / "wgtb"
+    if not (model.exists() and kernel.exists() and wgtb.exists()):
+        return None, "no trained model bundle (results/b200/model.json)"
+    t = {"int32": "INT32", "float32": "FLOAT32", "float64": "FLOAT64"}[dtype]
+    proc = subprocess.run([str(wgtb), "predict", "--model", str(model), "--kernel-json", str(kernel),
+                           "--dataset", f"{W}x{H}-{t}-{t}", "--device", "cuda"],
+                          capture_output=True, text=True, timeout=300)
+    if proc.returncode != 0:
+        return None, proc.stderr.strip()[-200:]
+    wc, wr = map(int, proc.stdout.split())
+    return (wc, wr), json.loads(model.read_text()).get("technique", "?")
+
+
 def quick_sweep(st, a, b, W, H):
     """Exhaustive wc x wr sweep of one pass (the tuner's oracle on this box):
     every even size with area <= 1024 (enumerate_space, space.cpp:134-145),
@@ -141,9 +159,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())  # --backend gloo may share one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     op, dtype, H1, W, iters, border, pad, (n, s, e, w) = CONFIGS[args.config]
     st = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w, border=border,
@@ -176,13 +198,25 @@ def run_ours(args):
                           "oracle_pass_ms": round(best_ms, 5),
                           "oracle_over_worst": round(worst / best_ms, 2),
                           "sweep_s": round(time.time() - t0, 1)}
+            pred, how = predict_block(args.config, W, shard.rows, dtype)
+            if pred:
+                pv = b[shard.north:shard.north + shard.rows]
+                pa = a[shard.north:shard.north + shard.rows]
+                pms = float(np.mean(st.time(pa, pv, pred[0], pred[1], samples=8, warmup=1,
+                                            flush_l2=True)))
+                sweep_info.update({"predicted_block": f"{pred[0]}x{pred[1]}", "technique": how,
+                                   "predicted_pass_ms": round(pms, 5),
+                                   "predicted_over_oracle": round(min(1.0, best_ms / pms), 4)})
+            else:
+                sweep_info["predicted_over_oracle"] = None
+                sweep_info["prediction_note"] = how
             for k in ((32, 4), (4, 4), (32, 8)):
                 if k in res:
                     sweep_info[f"perf_{k[0]}x{k[1]}"] = round(min(res.values()) / res[k], 4)
         else:
             wc = wr = 0
         if world > 1:
-            t = torch.tensor([wc, wr], device="cuda")
+            t = torch.tensor([wc, wr], device="cuda" if args.backend == "nccl" else "cpu")
             dist.broadcast(t, 0)
             wc, wr = int(t[0]), int(t[1])
     block = f"{wc}x{wr}"
@@ -211,7 +245,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cuda" if args.backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     launches = args.steps * iters
@@ -257,6 +292,7 @@ def run_ours(args):
                 "parallelism": f"row-shard x{world}" + (" + NCCL halo exchange" if world > 1 else ""),
             },
             "hbm_frac": round(achieved / peak, 4),
+            "predicted_over_oracle": sweep_info.get("predicted_over_oracle"),
             "tuning": sweep_info,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
@@ -316,7 +352,8 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
     for _ in range(k):
         once()
     dt = time.perf_counter() - t0
-    t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+    t = torch.tensor([dt], device="cuda" if dist.get_backend() == "nccl" else "cpu",
+                     dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t[0])
     nbytes = h_in.numel() * h_in.element_size()
@@ -420,6 +457,8 @@ def main():
     ap.add_argument("--wr", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="halo transport; gloo (host-staged) only to test the multi-rank path on 1 GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

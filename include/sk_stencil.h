@@ -97,6 +97,13 @@ typedef struct {
                           0 = auto, or 1, 2, 4, 8.  The workgroup (block) is
                           still wc x wr work-items; its tile covers
                           wc x (wr*K) cells.                                 */
+  int32_t fused_iterations; /* temporal blocking: TB generations per launch
+                          (0/1 = one pass per launch; 2 or 4 fuse TB passes in
+                          shared memory).  sk_stencil_launch
+                          then advances TB generations; sk_stencil_iterate
+                          splits `iterations` into fused launches + single
+                          passes.  Supported for five_point, heat, gol and
+                          boxmean on the TMA path.                            */
 } sk_stencil_desc;
 
 /* Launch one stencil pass over a W x H region, out-of-place, on `stream`
@@ -126,9 +133,11 @@ int sk_stencil_launch_custom(const sk_stencil_desc* desc, const sk_kernel_table*
                              int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
                              int64_t rows_below, int32_t wc, int32_t wr, void* stream);
 
-/* Iterated stencil: `iterations` passes ping-ponging between d_a (input) and
- * d_b.  The result lands in d_a when iterations is even, in d_b when odd;
- * *result_in_b (optional) says which.  Same pitch for both buffers. */
+/* Iterated stencil: `iterations` generations ping-ponging between d_a
+ * (input) and d_b, one launch per generation (or per TB generations when
+ * desc->fused_iterations = TB).  The result lands in d_a after an even
+ * number of launches, in d_b after an odd number; *result_in_b says which.
+ * Same pitch for both buffers. */
 int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
                        int64_t height, int64_t pitch, int32_t iterations, int32_t wc,
                        int32_t wr, void* stream, int32_t* result_in_b);

@@ -35,6 +35,7 @@ typedef struct {
   int32_t complexity, instructions;
   int32_t load_path;        /* ignored */
   int32_t cells_per_thread; /* ignored */
+  int32_t fused_iterations; /* ignored (one pass per call) */
 } oracle_desc;
 
 /* One pass over a W x H region (row pitch in elements); rows_above /

@@ -56,6 +56,7 @@ class sk_stencil_desc(ctypes.Structure):
         ("instructions", ctypes.c_int32),
         ("load_path", ctypes.c_int32),
         ("cells_per_thread", ctypes.c_int32),
+        ("fused_iterations", ctypes.c_int32),
     ]
 
 

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <memory>
 #include <mutex>
 
@@ -180,7 +181,10 @@ CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig&
             if (sk_buffers_equal(gold, g.out, static_cast<int64_t>(g.bytes), &equal) != SK_OK) {
               device_fail("sk_buffers_equal");
             }
-            mismatches += equal ? 0 : 1;
+            if (!equal) {
+              ++mismatches;
+              std::fprintf(stderr, "GOLD MISMATCH %s %s\n", s.id.c_str(), w.str().c_str());
+            }
           }
         }
       }

@@ -47,6 +47,13 @@ struct Geom {
   int stage_bytes;          // bytes per pipeline stage (128-aligned)
   int stages;               // TMA ring depth
   int box_h, nchunks;       // TMA box height and boxes per tile
+  // temporal blocking (fused.cuh): TB generations per launch.  When TB > 1
+  // the N/S/E/Wb above are the TB-scaled halo of the loaded box and
+  // bN/bS/bE/bW the stencil's own border region.
+  int TB;
+  int bN, bS, bE, bW;
+  int sp;                   // row pitch of the two scratch generation buffers
+  int scratch_elems;        // elements per scratch buffer (incl. K slack rows)
 };
 
 // ------------------------------------------------------------------ PTX glue
@@ -168,10 +175,14 @@ __device__ __forceinline__ void compute_tile(const T* tile, const Geom& g,
                                              const OpParams<T>& p, T (&res)[K]) {
   const Op op;
   const T* base = tile + (threadIdx.y * K + g.N) * g.tile_w + threadIdx.x + g.Wb;
+  if constexpr (has_column<Op>::value) {
+    op.template column<T, K>(base, g.tile_w, p, res);
+  } else {
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    TileView<T> view{base + j * g.tile_w, g.tile_w};
-    res[j] = op.template apply<T>(view, p);
+    for (int j = 0; j < K; ++j) {
+      TileView<T> view{base + j * g.tile_w, g.tile_w};
+      res[j] = op.template apply<T>(view, p);
+    }
   }
 }
 

@@ -2,4 +2,5 @@
 #include <cstdint>
 #define SK_T float
 #define SK_REGISTRY_FN kernels_f32
+#define SK_FUSED_FN fused_f32
 #include "kernels_inst.cuh"

@@ -2,4 +2,5 @@
 #include <cstdint>
 #define SK_T double
 #define SK_REGISTRY_FN kernels_f64
+#define SK_FUSED_FN fused_f64
 #include "kernels_inst.cuh"

@@ -1,6 +1,7 @@
 // Instantiates every (op, K) kernel pair for one element type SK_T and
 // defines the registry function SK_REGISTRY_FN (see registry.cuh).
 #include "kernels.cuh"
+#include "fused.cuh"
 #include "registry.cuh"
 
 namespace sk {
@@ -22,7 +23,35 @@ KernelPair pair_for_k(int K) {
   }
 }
 
+template <class Op, typename T, int K>
+KernelPtr fused_for_tb(int TB) {
+  return TB == 2 ? reinterpret_cast<KernelPtr>(&k_stencil_tma_fused<Op, T, K, 2, 1024>)
+                 : reinterpret_cast<KernelPtr>(&k_stencil_tma_fused<Op, T, K, 4, 1024>);
+}
+
+template <class Op, typename T>
+KernelPtr fused_for(int K, int TB) {
+  switch (K) {
+    case 1: return fused_for_tb<Op, T, 1>(TB);
+    case 2: return fused_for_tb<Op, T, 2>(TB);
+    case 4: return fused_for_tb<Op, T, 4>(TB);
+    default: return fused_for_tb<Op, T, 8>(TB);
+  }
+}
+
 }  // namespace
+
+KernelPtr SK_FUSED_FN(const sk_stencil_desc& d, int K, int TB) {
+  using T = SK_T;
+  if (TB != 2 && TB != 4) return nullptr;
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return fused_for<FivePoint, T>(K, TB);
+    case SK_OP_HEAT: return fused_for<Heat, T>(K, TB);
+    case SK_OP_GOL: return fused_for<Gol, T>(K, TB);
+    case SK_OP_BOXMEAN: return fused_for<BoxMean, T>(K, TB);
+    default: return nullptr;
+  }
+}
 
 KernelPair SK_REGISTRY_FN(const sk_stencil_desc& d, int K) {
   using T = SK_T;

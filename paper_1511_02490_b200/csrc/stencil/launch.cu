@@ -157,6 +157,10 @@ int validate_desc(const sk_stencil_desc* d) {
       d->cells_per_thread != 4 && d->cells_per_thread != 8) {
     return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
   }
+  if (d->fused_iterations != 0 && d->fused_iterations != 1 && d->fused_iterations != 2 &&
+      d->fused_iterations != 4) {
+    return fail(SK_EINVAL, "fused_iterations must be 0, 1, 2 or 4");
+  }
   int need = 0;
   switch (d->op) {
     case SK_OP_FIVE_POINT: case SK_OP_HEAT: case SK_OP_GOL: case SK_OP_SOBEL: case SK_OP_NMS:
@@ -181,6 +185,14 @@ int validate_desc(const sk_stencil_desc* d) {
 }
 
 // --------------------------------------------------------- kernel registry
+KernelPtr fused_for_desc(const sk_stencil_desc& d, int K, int TB) {
+  switch (d.dtype) {
+    case SK_INT32: return fused_i32(d, K, TB);
+    case SK_FLOAT32: return fused_f32(d, K, TB);
+    default: return fused_f64(d, K, TB);
+  }
+}
+
 KernelPair kernels_for_desc(const sk_stencil_desc& d, int K) {
   switch (d.dtype) {
     case SK_INT32: return kernels_i32(d, K);
@@ -391,9 +403,17 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   if (!kp.tma || !kp.explicit_) return fail(SK_EINVAL, "kernel table has no entry for K=%d", K);
   const bool drv = custom != nullptr;
   plan->driver_handle = drv;
+  // temporal blocking: TB generations per launch (TMA path only)
+  const int TB = (!drv && d.fused_iterations > 1) ? d.fused_iterations : 1;
+  if (TB > 1) {
+    kp.tma = fused_for_desc(d, K, TB);
+    if (!kp.tma) return fail(SK_ENOTSUP, "no fused (TB=%d) kernel for op %d", TB, d.op);
+  }
   KernelAttr a_tma, a_exp;
   if (int rc = kernel_attr(dev, kp.tma, info, &a_tma, drv)) return rc;
   if (int rc = kernel_attr(dev, kp.explicit_, info, &a_exp, drv)) return rc;
+  // halo of the loaded box: TB border regions
+  const int eN = TB * d.north, eS = TB * d.south, eE = TB * d.east, eW = TB * d.west;
 
   const long long threads = static_cast<long long>(wc) * wr;
   const size_t es = dtype_size(d.dtype);
@@ -402,31 +422,36 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   g.H = static_cast<int>(H);
   g.pitch_in = pitch_in;
   g.pitch_out = pitch_out;
-  g.above = static_cast<int>(std::min<long long>(above, d.north));
-  g.below = static_cast<int>(std::min<long long>(below, d.south));
-  g.N = d.north;
-  g.S = d.south;
-  g.E = d.east;
-  g.Wb = d.west;
+  g.above = static_cast<int>(std::min<long long>(above, eN));
+  g.below = static_cast<int>(std::min<long long>(below, eS));
+  g.N = eN;
+  g.S = eS;
+  g.E = eE;
+  g.Wb = eW;
+  g.TB = TB;
+  g.bN = d.north;
+  g.bS = d.south;
+  g.bE = d.east;
+  g.bW = d.west;
   g.wc = wc;
   g.wr = wr;
   g.K = K;
   g.tile_rows = wr * K;
-  g.lw = wc + d.east + d.west;
+  g.lw = wc + eE + eW;
   const int vec = static_cast<int>(16 / es);
   g.vec = vec;
   // Box width: the logical tile plus the largest 16-B alignment offset any
   // tile can have (constant when wc is a multiple of vec).
-  const int max_off = (wc % vec == 0) ? ((-d.west) & (vec - 1)) : vec - 1;
+  const int max_off = (wc % vec == 0) ? ((-eW) & (vec - 1)) : vec - 1;
   g.tile_w = (g.lw + max_off + vec - 1) / vec * vec;
-  g.tile_h = g.tile_rows + d.north + d.south;
+  g.tile_h = g.tile_rows + eN + eS;
   g.tiles_x = static_cast<int>((W + wc - 1) / wc);
   g.tiles_y = static_cast<int>((H + g.tile_rows - 1) / g.tile_rows);
   // Interior tiles: read only inside the readable window and store in range.
-  g.ex_lo = static_cast<int>(ceil_div(d.west, wc));
-  g.ex_hi = static_cast<int>(floor_div(W - wc - d.east, wc));
-  g.ey_lo = static_cast<int>(ceil_div(std::max<long long>(0, d.north - g.above), g.tile_rows));
-  g.ey_hi = static_cast<int>(floor_div(H + g.below - d.south - g.tile_rows, g.tile_rows));
+  g.ex_lo = static_cast<int>(ceil_div(eW, wc));
+  g.ex_hi = static_cast<int>(floor_div(W - wc - eE, wc));
+  g.ey_lo = static_cast<int>(ceil_div(std::max<long long>(0, eN - g.above), g.tile_rows));
+  g.ey_hi = static_cast<int>(floor_div(H + g.below - eS - g.tile_rows, g.tile_rows));
   g.mode = d.border_mode;
   g.pad_is_zero = d.pad_value == 0.0 && !std::signbit(d.pad_value);
   plan->tile_bytes = static_cast<long long>(g.lw) * g.tile_h * static_cast<long long>(es);
@@ -436,6 +461,10 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
                 (in == nullptr || (reinterpret_cast<uintptr_t>(in) % 16) == 0) &&
                 static_cast<long long>(g.tiles_x) * g.tiles_y < (1LL << 31);
   bool use_tma = d.load_path == SK_LOAD_TMA || (d.load_path == SK_LOAD_AUTO && tma_ok);
+  if (TB > 1) {
+    if (!tma_ok) return fail(SK_ENOTSUP, "fused iterations need the TMA path (tile_w %d)", g.tile_w);
+    use_tma = true;
+  }
   if (d.load_path == SK_LOAD_TMA && !tma_ok) {
     return fail(SK_ENOTSUP, "TMA path not possible for this tile/buffer (tile_w %d)", g.tile_w);
   }
@@ -471,23 +500,37 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   g.nchunks = (g.tile_h + 255) / 256;
   g.box_h = (g.tile_h + g.nchunks - 1) / g.nchunks;
   if (g.nchunks > 1) g.box_h = (g.box_h + 7) / 8 * 8;
-  long long stage = static_cast<long long>(g.tile_w) * g.box_h * g.nchunks *
+  // fused kernels read up to K-1 rows past a generation region: slack rows
+  const int slack = TB > 1 ? K : 0;
+  long long stage = static_cast<long long>(g.tile_w) * (g.box_h * g.nchunks + slack) *
                     static_cast<long long>(es);
   stage = (stage + 127) / 128 * 128;
-  if (stage + 128 > attr.max_dyn_smem) {
-    return fail(SK_REFUSED, "tile %lld B exceeds shared memory %d B", stage, attr.max_dyn_smem);
+  long long scratch = 0;
+  if (TB > 1) {
+    g.sp = wc + (TB - 1) * (d.east + d.west);
+    const long long rows = g.tile_rows + static_cast<long long>(TB - 1) * (d.north + d.south) + K;
+    g.scratch_elems = static_cast<int>((g.sp * rows + 31) / 32 * 32);
+    scratch = 2LL * g.scratch_elems * static_cast<long long>(es);
+  } else {
+    g.sp = 0;
+    g.scratch_elems = 0;
+  }
+  if (stage + scratch + 128 > attr.max_dyn_smem) {
+    return fail(SK_REFUSED, "tile %lld B exceeds shared memory %d B", stage + scratch,
+                attr.max_dyn_smem);
   }
   g.stage_bytes = static_cast<int>(stage);
   // Ring depth: as deep as the per-block share of the SM's shared memory
   // allows at the thread-limited occupancy, between 2 and 8 stages.
   int occ2 = occupancy(dev, plan->kernel, plan->threads,
-                       static_cast<int>(std::min<long long>(2 * stage + 128, attr.max_dyn_smem)), drv);
+                       static_cast<int>(std::min<long long>(2 * stage + scratch + 128, attr.max_dyn_smem)),
+                       drv);
   int blocks = std::max(1, occ2);
-  long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 128;
+  long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 128 - scratch;
   int stages = static_cast<int>(std::clamp<long long>(share / stage, 1, 8));
-  while (stages > 1 && stage * stages + 128 > attr.max_dyn_smem) --stages;
+  while (stages > 1 && stage * stages + scratch + 128 > attr.max_dyn_smem) --stages;
   g.stages = stages;
-  plan->smem = static_cast<int>(stage * stages + 16 * stages);  // + full/empty barriers
+  plan->smem = static_cast<int>(stage * stages + scratch + 16 * stages);  // + full/empty barriers
   int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem, drv);
   if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
   long long ntiles = static_cast<long long>(g.tiles_x) * g.tiles_y;
@@ -668,14 +711,21 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
   if (iterations < 0) return fail(SK_EINVAL, "negative iterations");
   void* src = d_a;
   void* dst = d_b;
-  for (int i = 0; i < iterations; ++i) {
-    if (int rc = launch(*desc, src, dst, width, height, pitch, pitch, 0, 0, wc, wr,
+  int launches = 0;
+  const int TB = desc->fused_iterations > 1 ? desc->fused_iterations : 1;
+  sk_stencil_desc one = *desc;
+  one.fused_iterations = 0;
+  for (int done = 0; done < iterations; ++launches) {
+    // TB generations per fused launch; the remainder one pass at a time
+    const bool fuse = TB > 1 && iterations - done >= TB;
+    if (int rc = launch(fuse ? *desc : one, src, dst, width, height, pitch, pitch, 0, 0, wc, wr,
                         static_cast<cudaStream_t>(stream))) {
       return rc;
     }
+    done += fuse ? TB : 1;
     std::swap(src, dst);
   }
-  if (result_in_b) *result_in_b = (iterations % 2) == 1;
+  if (result_in_b) *result_in_b = (launches % 2) == 1;
   return SK_OK;
 }
 

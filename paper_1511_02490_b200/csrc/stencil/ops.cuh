@@ -87,9 +87,40 @@ struct Heat {
   }
 };
 
+// Ops may also provide a column form evaluating a work-item's K vertically
+// adjacent cells at once (kColumn = true): `column<T, K>(centre, pitch, p, res)`
+// with centre = the first cell.  It must equal K calls of apply() exactly.
+template <class Op, class = void>
+struct has_column : std::false_type {};
+template <class Op>
+struct has_column<Op, std::void_t<decltype(Op::kColumn)>> : std::bool_constant<Op::kColumn> {};
+
 // ----------------------------------------------------------------------- gol
 // Conway B3/S23 on the 3x3 Moore neighbourhood; a cell is alive iff != 0.
+// Column form: the alive count of row i over columns c-1..c+1 is shared by
+// the three cells i-1, i, i+1 of the work-item's column (same integer count).
 struct Gol {
+  static constexpr bool kColumn = true;
+
+  template <typename T, int K>
+  __device__ __forceinline__ void column(const T* centre, int pitch, const OpParams<T>&,
+                                         T (&res)[K]) const {
+    int mid[K + 2];
+    int row[K + 2];
+#pragma unroll
+    for (int i = 0; i < K + 2; ++i) {
+      const T* r = centre + (i - 1) * pitch;
+      const int l = r[-1] != T(0), m = r[0] != T(0), rr = r[1] != T(0);
+      mid[i] = m;
+      row[i] = l + m + rr;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int n = row[k] + row[k + 1] + row[k + 2] - mid[k + 1];
+      res[k] = (n == 3 || (mid[k + 1] && n == 2)) ? T(1) : T(0);
+    }
+  }
+
   template <typename T, class V>
   __device__ __forceinline__ T apply(const V& v, const OpParams<T>&) const {
     int n = (v.at(-1, -1) != T(0)) + (v.at(-1, 0) != T(0)) + (v.at(-1, 1) != T(0)) +

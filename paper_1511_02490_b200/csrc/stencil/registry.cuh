@@ -19,4 +19,10 @@ KernelPair kernels_i32(const sk_stencil_desc& d, int K);
 KernelPair kernels_f32(const sk_stencil_desc& d, int K);
 KernelPair kernels_f64(const sk_stencil_desc& d, int K);
 
+// Temporal-blocking kernels (TMA only): TB in {2, 4}; nullptr when the op has
+// no fused instantiation.
+KernelPtr fused_i32(const sk_stencil_desc& d, int K, int TB);
+KernelPtr fused_f32(const sk_stencil_desc& d, int K, int TB);
+KernelPtr fused_f64(const sk_stencil_desc& d, int K, int TB);
+
 }  // namespace sk

@@ -73,8 +73,24 @@ class RowShard:
         return buf[self.north:self.north + self.rows]
 
 
+def _staged_exchange(buf: torch.Tensor, shard: RowShard, group=None) -> None:
+    """gloo cannot move CUDA tensors: stage the halo slices through host
+    memory (used only to exercise the multi-rank path on a single GPU)."""
+    cpu = torch.empty((shard.buffer_rows, buf.shape[1]), dtype=buf.dtype)
+    n, s, h = shard.north, shard.south, shard.rows
+    cpu[n:n + h].copy_(buf[n:n + h])
+    exchange_halos(cpu, shard, group)
+    if shard.rank > 0 and n:
+        buf[0:n].copy_(cpu[0:n])
+    if shard.rank < shard.world - 1 and s:
+        buf[n + h:n + h + s].copy_(cpu[n + h:n + h + s])
+
+
 def exchange_halos(buf: torch.Tensor, shard: RowShard, group=None) -> None:
     """Fill the north/south halo rows of `buf` from the neighbouring ranks."""
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        _staged_exchange(buf, shard, group)
+        return
     n, s, h = shard.north, shard.south, shard.rows
     ops = []
     if shard.rank > 0:

@@ -64,6 +64,7 @@ class Stencil:
     instructions: int = 100      # synthetic kernels only
     load_path: str = "auto"      # "auto" | "tma" | "explicit"
     cells_per_thread: int = 0    # K cells per work-item; 0 = auto
+    fused_iterations: int = 0    # temporal blocking: generations per launch (0/1, 2, 4)
     _desc: N.sk_stencil_desc = field(init=False, repr=False)
 
     def __post_init__(self):
@@ -77,7 +78,8 @@ class Stencil:
             instructions=int(self.instructions),
             load_path={"auto": N.SK_LOAD_AUTO, "tma": N.SK_LOAD_TMA,
                        "explicit": N.SK_LOAD_EXPLICIT}[self.load_path],
-            cells_per_thread=int(self.cells_per_thread))
+            cells_per_thread=int(self.cells_per_thread),
+            fused_iterations=int(self.fused_iterations))
 
     # -- construction from reference descriptors ---------------------------
     @classmethod

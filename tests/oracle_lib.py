@@ -27,7 +27,8 @@ class oracle_desc(ctypes.Structure):
                 ("south", ctypes.c_int32), ("east", ctypes.c_int32), ("west", ctypes.c_int32),
                 ("border_mode", ctypes.c_int32), ("pad_value", ctypes.c_double),
                 ("complexity", ctypes.c_int32), ("instructions", ctypes.c_int32),
-                ("load_path", ctypes.c_int32), ("cells_per_thread", ctypes.c_int32)]
+                ("load_path", ctypes.c_int32), ("cells_per_thread", ctypes.c_int32),
+                ("fused_iterations", ctypes.c_int32)]
 
 
 def lib():

@@ -22,8 +22,8 @@ def test_prototypes_cover_header():
 
 
 def test_descriptor_layout_matches_header():
-    # int32 x7 (+4 pad), double at 32, int32 x4 -> 56 bytes
-    assert ctypes.sizeof(N.sk_stencil_desc) == 56
+    # int32 x7 (+4 pad), double at 32, int32 x5 (+4 pad) -> 64 bytes
+    assert ctypes.sizeof(N.sk_stencil_desc) == 64
     assert N.sk_stencil_desc.pad_value.offset == 32
 
 
