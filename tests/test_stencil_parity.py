@@ -257,3 +257,51 @@ def test_every_legal_size_matches_gold_standard(op, dtype, borders, border):
         torch.cuda.synchronize()
     bad = [k for k, b in outs.items() if b.cpu().numpy().tobytes() != want.tobytes()]
     assert not bad, f"{len(bad)} sizes differ, e.g. {bad[:5]}"
+
+
+FUSED_CASES = [
+    ("gol", "int32", (1, 1, 1, 1), "pad", 0.0),
+    ("heat", "float32", (1, 1, 1, 1), "nearest", 0.0),
+    ("five_point", "float64", (1, 1, 1, 1), "pad", 1.0),
+    ("boxmean", "float32", (3, 2, 1, 0), "nearest", 0.0),
+    ("boxmean", "int32", (1, 2, 2, 1), "pad", 7.0),
+]
+
+
+@pytest.mark.parametrize("op,dtype,borders,border,pad", FUSED_CASES)
+@pytest.mark.parametrize("tb", [2, 4])
+@pytest.mark.parametrize("k", [0, 1, 8])
+def test_fused_iterations_vs_oracle(op, dtype, borders, border, pad, tb, k):
+    """Temporal blocking (TB generations per launch) must equal TB one-pass
+    generations exactly, including the per-generation border semantics."""
+    n, s, e, w = borders
+    st = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w, border=border,
+                 pad_value=pad, cells_per_thread=k, fused_iterations=tb)
+    x = rand_grid(dtype, (157, 200), 21, op)
+    iters = 2 * tb + 1  # fused launches + a one-pass remainder
+    want = O.iterate(O.desc_from_stencil(st), x, iters)
+    for wc, wr in [(32, 8), (16, 16), (64, 2), (6, 10), (128, 4)]:
+        if st.probe(200, 157, wc, wr)["status"] != "OK":
+            continue
+        a, b = to_dev(x), torch.empty_like(to_dev(x))
+        got = st.iterate(a, b, iters, wc, wr).cpu().numpy()
+        assert_same(got, want, f"fused TB={tb} K={k} {op}/{dtype} {wc}x{wr}")
+
+
+def test_fused_single_launch_advances_tb_generations():
+    st = Stencil(op="gol", dtype="int32", fused_iterations=4)
+    x = rand_grid("int32", (256, 256), 3, "gol")
+    want = O.iterate(O.desc_from_stencil(st), x, 4)
+    a = to_dev(x)
+    b = torch.empty_like(a)
+    st(a, b, 32, 8)
+    torch.cuda.synchronize()
+    assert b.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_fused_unsupported_op_is_enotsup():
+    from paper_1511_02490_b200 import NativeError
+    st = Stencil(op="sobel", dtype="float32", fused_iterations=2)
+    a = to_dev(rand_grid("float32", (64, 64), 1))
+    with pytest.raises(NativeError):
+        st(a, torch.empty_like(a), 32, 8)
