@@ -296,9 +296,14 @@ __global__ void __launch_bounds__(MAXT)
     }
     T res[K];
     compute_tile<Op, T, K>(tile, g, p, res);
+    store_tile<T, K>(out, g, r0, c0, edge, res);
+    // Release the stage only after the stores: they consume every value the
+    // warp loaded from it, so no shared-memory read of this tile can still be
+    // in flight when the producer's TMA refill overwrites the stage.  (An
+    // arrive issued right after the loads raced the refill: ~17% of runs on
+    // heat 2048^2 at 2x32, K=2, 2-stage ring - scripts/stress_race.py.)
     __syncwarp(warp_mask);
     if (lane == 0) mbar_arrive(&empty[s]);
-    store_tile<T, K>(out, g, r0, c0, edge, res);
 
     tx += step_x;
     ty += step_y;

@@ -305,3 +305,23 @@ def test_fused_unsupported_op_is_enotsup():
     a = to_dev(rand_grid("float32", (64, 64), 1))
     with pytest.raises(NativeError):
         st(a, torch.empty_like(a), 32, 8)
+
+
+def test_stage_release_race_regression():
+    """Regression: the warp released its TMA ring stage (mbarrier arrive)
+    before its shared-memory loads had returned, so a refill could overwrite
+    cells still being read - 523/3000 runs wrong on this exact configuration
+    (2-stage ring, K=2, refills on every tile).  The arrive now follows the
+    stores, which consume every loaded value."""
+    st = Stencil(op="heat", dtype="float32", border="nearest")
+    x = rand_grid("float32", (2048, 2048), 1)
+    want = to_dev(O.stencil(O.desc_from_stencil(st), x))
+    a = to_dev(x)
+    outs = [torch.empty_like(a) for _ in range(4)]
+    bad = 0
+    for i in range(600):
+        b = outs[i % 4]
+        st(a, b, 2, 32)
+        if i % 4 == 3:
+            bad += sum(int(not torch.equal(o, want)) for o in outs)
+    assert bad == 0
