@@ -10,7 +10,7 @@
 //                  --technique T|all --partition kfold|synthreal|loo-kernel|loo-dataset|loo-device
 //                  [--folds 10] [--seed S] [--metrics out.csv] [--pin-baseline WxH] [--expert]
 //   wgtb train     --scenarios DIR --samples F --refused F --contexts F --technique T --out model.json
-//   wgtb predict   --model model.json --kernel-json F --dataset WxH-IN-OUT [--device cuda|fixture:ID]
+//   wgtb predict   --model model.json --kernel-json F --dataset WxH-IN-OUT [--device cuda|fixture:ID|json:PATH]
 //                  [--refused F --contexts F]   (prints "wc wr")
 //   wgtb features  [--device 0]                 (cudaDeviceProp -> DeviceDescriptor JSON)
 //
@@ -279,6 +279,9 @@ int cmd_train(const Args& a) {
 int cmd_predict(const Args& a) {
   const nlohmann::json bundle = nlohmann::json::parse(read_text(a.need("--model")));
   DeviceDescriptor dev = a.get("--device", "cuda") == "cuda" ? device_from_cuda(0) : DeviceDescriptor{};
+  if (a.get("--device", "cuda").starts_with("json:")) {
+    dev = device_from_json(nlohmann::json::parse(read_text(a.get("--device").substr(5))));
+  }
   if (a.get("--device", "cuda").starts_with("fixture:")) {
     const std::string id = a.get("--device").substr(8);
     for (const auto& d : reference_devices()) {
