@@ -154,7 +154,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1511_02490_b200 import Stencil
-    from paper_1511_02490_b200.distributed import RowShard, cuda_step, iterate_sharded
+    from paper_1511_02490_b200.distributed import (RowShard, cuda_step, iterate_sharded,
+                                                   iterate_sharded_overlapped)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -225,6 +226,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def one_step():
+        if world > 1 and not args.no_overlap:
+            return iterate_sharded_overlapped(a, b, shard, iters, st, wc, wr)
         return iterate_sharded(a, b, shard, iters, step_fn)
 
     for _ in range(args.warmup):
@@ -457,6 +460,8 @@ def main():
     ap.add_argument("--wr", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N>1: exchange halos between passes instead of behind the interior")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="halo transport; gloo (host-staged) only to test the multi-rank path on 1 GPU")
     args = ap.parse_args()

@@ -17,7 +17,8 @@ import torch.distributed as dist
 
 import oracle_lib as O
 from paper_1511_02490_b200 import Stencil
-from paper_1511_02490_b200.distributed import RowShard, cuda_step, iterate_sharded, scatter_rows
+from paper_1511_02490_b200.distributed import (RowShard, cuda_step, iterate_sharded,
+                                               iterate_sharded_overlapped, scatter_rows)
 
 
 def main():
@@ -40,13 +41,19 @@ def main():
         res = iterate_sharded(a, b, shard, iters, cuda_step(st, 32, 4))
         torch.cuda.synchronize()
         part = shard.owned(res).cpu()
+        a2 = scatter_rows(torch.from_numpy(full).cuda(), shard)
+        b2 = torch.zeros_like(a2)
+        res2 = iterate_sharded_overlapped(a2, b2, shard, iters, st, 32, 4)
+        torch.cuda.synchronize()
+        same_overlap = bool(torch.equal(shard.owned(res2), shard.owned(res)))
         parts = [None] * world
-        dist.all_gather_object(parts, (shard.r0, part.numpy()))
+        dist.all_gather_object(parts, (shard.r0, part.numpy(), same_overlap))
         if rank == 0:
             got = np.concatenate([p[1] for p in sorted(parts, key=lambda t: t[0])])
             want = O.iterate(O.desc_from_stencil(st), full, iters)
-            same = got.tobytes() == want.tobytes()
-            print(f"{op}: {'match' if same else 'MISMATCH'}", flush=True)
+            same = got.tobytes() == want.tobytes() and all(p[2] for p in parts)
+            print(f"{op}: {'match' if same else 'MISMATCH'} (overlapped: {[p[2] for p in parts]})",
+                  flush=True)
             ok = ok and same
     if rank == 0:
         print("ALL_OK" if ok else "FAILED", flush=True)
