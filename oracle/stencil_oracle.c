@@ -30,7 +30,8 @@ typedef struct {
   char* out;
   int64_t W, H, pin, pout, above, below;
   int64_t r_begin, r_end;
-  double gw[21 * 21];      /* gaussian weights, float kernels */
+  double gw[21 * 21];      /* unused (kept for layout) */
+  double gb[21];           /* gaussian 1-D weights C(2g,j)/2^(2g) */
   long long giw[21 * 21];  /* gaussian weights, int kernels    */
 } job;
 
@@ -91,21 +92,27 @@ static float cell_f32(const job* j, int64_t r, int64_t c) {
       int alive = V(0, 0) != 0.0f;
       return (n == 3 || (alive && n == 2)) ? 1.0f : 0.0f;
     }
-    case OP_BOXMEAN: {
+    case OP_BOXMEAN: { /* sum of row sums (west->east), rows north->south */
       float s = 0.0f;
-      for (int dr = -d->north; dr <= d->south; ++dr)
-        for (int dc = -d->west; dc <= d->east; ++dc) s = s + V(dr, dc);
+      for (int dr = -d->north; dr <= d->south; ++dr) {
+        float row = V(dr, -d->west);
+        for (int dc = -d->west + 1; dc <= d->east; ++dc) row = row + V(dr, dc);
+        s = dr == -d->north ? row : s + row;
+      }
       return s / (float)((d->north + d->south + 1) * (d->east + d->west + 1));
     }
-    case OP_GAUSSIAN: {
-      int g = d->north, n = 2 * g + 1;
+    case OP_GAUSSIAN: { /* separable: row pass west->east, then rows north->south */
+      int g = d->north;
       float s = 0.0f;
-      for (int i = -g; i <= g; ++i)
-        for (int k = -g; k <= g; ++k) {
-          float w = (float)j->gw[(i + g) * n + (k + g)];
-          float p = w * V(i, k);
-          s = s + p;
+      for (int i = -g; i <= g; ++i) {
+        float row = (float)j->gb[0] * V(i, -g);
+        for (int k = -g + 1; k <= g; ++k) {
+          float p = (float)j->gb[k + g] * V(i, k);
+          row = row + p;
         }
+        float t = (float)j->gb[i + g] * row;
+        s = i == -g ? t : s + t;
+      }
       return s;
     }
     case OP_SOBEL: {
@@ -180,20 +187,27 @@ static double cell_f64(const job* j, int64_t r, int64_t c) {
       int alive = V(0, 0) != 0.0;
       return (n == 3 || (alive && n == 2)) ? 1.0 : 0.0;
     }
-    case OP_BOXMEAN: {
+    case OP_BOXMEAN: { /* sum of row sums (west->east), rows north->south */
       double s = 0.0;
-      for (int dr = -d->north; dr <= d->south; ++dr)
-        for (int dc = -d->west; dc <= d->east; ++dc) s = s + V(dr, dc);
+      for (int dr = -d->north; dr <= d->south; ++dr) {
+        double row = V(dr, -d->west);
+        for (int dc = -d->west + 1; dc <= d->east; ++dc) row = row + V(dr, dc);
+        s = dr == -d->north ? row : s + row;
+      }
       return s / (double)((d->north + d->south + 1) * (d->east + d->west + 1));
     }
-    case OP_GAUSSIAN: {
-      int g = d->north, n = 2 * g + 1;
+    case OP_GAUSSIAN: { /* separable: row pass west->east, then rows north->south */
+      int g = d->north;
       double s = 0.0;
-      for (int i = -g; i <= g; ++i)
-        for (int k = -g; k <= g; ++k) {
-          double p = j->gw[(i + g) * n + (k + g)] * V(i, k);
-          s = s + p;
+      for (int i = -g; i <= g; ++i) {
+        double row = j->gb[0] * V(i, -g);
+        for (int k = -g + 1; k <= g; ++k) {
+          double p = j->gb[k + g] * V(i, k);
+          row = row + p;
         }
+        double t = j->gb[i + g] * row;
+        s = i == -g ? t : s + t;
+      }
       return s;
     }
     case OP_SOBEL: {
@@ -360,6 +374,7 @@ int oracle_stencil(const oracle_desc* d, const void* in, void* out, int64_t widt
         base.giw[i * n + k] = cij;
         base.gw[i * n + k] = ldexp((double)cij, -4 * g);
       }
+    for (int i = 0; i < n; ++i) base.gb[i] = ldexp((double)binom(2 * g, i), -2 * g);
   }
   job* jobs = (job*)malloc(sizeof(job) * (size_t)nt);
   pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nt);

@@ -64,7 +64,9 @@ KernelPair SK_REGISTRY_FN(const sk_stencil_desc& d, int K) {
         return pair_for_k<BoxMeanFixed<5, 1, 3, 0>, T>(K);
       }
       return pair_for_k<BoxMean, T>(K);
-    case SK_OP_GAUSSIAN: return pair_for_k<Gaussian, T>(K);
+    case SK_OP_GAUSSIAN:
+      if (d.north == 5) return pair_for_k<GaussianFixed<5>, T>(K);
+      return pair_for_k<Gaussian, T>(K);
     case SK_OP_SOBEL: return pair_for_k<Sobel, T>(K);
     case SK_OP_NMS: return pair_for_k<Nms, T>(K);
     case SK_OP_THRESHOLD: return pair_for_k<Threshold, T>(K);

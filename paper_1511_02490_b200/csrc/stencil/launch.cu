@@ -123,17 +123,14 @@ void fill_params(const sk_stencil_desc& d, OpParams<T>* p) {
   p->alu_iters = d.op == SK_OP_SYNTHETIC ? (d.complexity ? d.instructions / 4 : d.instructions / 32)
                                          : 0;
   if (d.op == SK_OP_GAUSSIAN) {
-    int g = d.north;
+    const int g = d.north;
     p->gauss_radius = g;
-    int n = 2 * g + 1;
-    for (int i = 0; i < n; ++i) {
-      for (int j = 0; j < n; ++j) {
-        long long cij = binom(2 * g, i) * binom(2 * g, j);
-        if constexpr (std::is_same_v<T, int32_t>) {
-          p->gauss_w[i * n + j] = cij;
-        } else {
-          p->gauss_w[i * n + j] = static_cast<T>(std::ldexp(static_cast<double>(cij), -4 * g));
-        }
+    for (int j = 0; j <= 2 * g; ++j) {
+      const long long c = binom(2 * g, j);
+      if constexpr (std::is_same_v<T, int32_t>) {
+        p->gauss_b[j] = c;
+      } else {
+        p->gauss_b[j] = static_cast<T>(std::ldexp(static_cast<double>(c), -2 * g));
       }
     }
   }

@@ -28,7 +28,7 @@ struct OpParams {
   int complexity;
   int alu_iters;                 // synthetic: dependent ALU iterations per cell
   int gauss_radius;              // gaussian: g
-  WeightT<T> gauss_w[21 * 21];   // gaussian: row-major (2g+1)^2 weights
+  WeightT<T> gauss_b[21];        // gaussian: 1-D binomial weights b_j, j = -g..g
 };
 
 // Integer accumulator for int32 stencils: wraps modulo 2^64 so overflow is
@@ -132,70 +132,150 @@ struct Gol {
 };
 
 // ------------------------------------------------------------------- boxmean
-// Sum of the whole border region, rows north..south outer, columns west..east
-// inner, then float: sum / count, int: sum / count (truncating).
+// Sum of row sums: each row of the region is summed west to east, then the
+// row sums north to south; divided by the cell count (int: truncating).
+// The column form shares every row sum between the K cells of a work-item.
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type acc_add(typename Acc<T>::type a, T b) {
+  if constexpr (std::is_same_v<T, int32_t>) return wrap_add(a, b);
+  else return a + b;
+}
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type acc_add2(typename Acc<T>::type a,
+                                                          typename Acc<T>::type b) {
+  if constexpr (std::is_same_v<T, int32_t>) return wrap_add(a, b);
+  else return a + b;
+}
+template <typename T>
+__device__ __forceinline__ T acc_div(typename Acc<T>::type s, int count) {
+  if constexpr (std::is_same_v<T, int32_t>) return static_cast<int32_t>(s / count);
+  else return s / T(count);
+}
+
 struct BoxMean {
   template <typename T, class V>
   __device__ __forceinline__ T apply(const V& v, const OpParams<T>& p) const {
     using A = typename Acc<T>::type;
     A s = A(0);
     for (int dr = -p.north; dr <= p.south; ++dr) {
-      for (int dc = -p.west; dc <= p.east; ++dc) {
-        if constexpr (std::is_same_v<T, int32_t>) s = wrap_add(s, v.at(dr, dc));
-        else s = s + v.at(dr, dc);
-      }
+      A row = A(v.at(dr, -p.west));
+      for (int dc = -p.west + 1; dc <= p.east; ++dc) row = acc_add<T>(row, v.at(dr, dc));
+      s = dr == -p.north ? row : acc_add2<T>(s, row);
     }
-    int count = (p.north + p.south + 1) * (p.east + p.west + 1);
-    if constexpr (std::is_same_v<T, int32_t>) return static_cast<int32_t>(s / count);
-    else return s / T(count);
+    return acc_div<T>(s, (p.north + p.south + 1) * (p.east + p.west + 1));
   }
 };
 
-// Asymmetric (5,1,3,0) box mean with compile-time extents: the BASELINE
-// config-4 kernel.  Same arithmetic and summation order as BoxMean.
+// Compile-time extents (the BASELINE config-4 (5,1,3,0) kernel).
 template <int N, int S, int E, int W>
 struct BoxMeanFixed {
+  static constexpr bool kColumn = true;
+  static constexpr int kCount = (N + S + 1) * (E + W + 1);
+
+  template <typename T>
+  __device__ __forceinline__ typename Acc<T>::type row_sum(const T* r) const {
+    using A = typename Acc<T>::type;
+    A row = A(r[-W]);
+#pragma unroll
+    for (int dc = -W + 1; dc <= E; ++dc) row = acc_add<T>(row, r[dc]);
+    return row;
+  }
+
   template <typename T, class V>
   __device__ __forceinline__ T apply(const V& v, const OpParams<T>&) const {
     using A = typename Acc<T>::type;
     A s = A(0);
 #pragma unroll
     for (int dr = -N; dr <= S; ++dr) {
+      A row = A(v.at(dr, -W));
 #pragma unroll
-      for (int dc = -W; dc <= E; ++dc) {
-        if constexpr (std::is_same_v<T, int32_t>) s = wrap_add(s, v.at(dr, dc));
-        else s = s + v.at(dr, dc);
-      }
+      for (int dc = -W + 1; dc <= E; ++dc) row = acc_add<T>(row, v.at(dr, dc));
+      s = dr == -N ? row : acc_add2<T>(s, row);
     }
-    constexpr int count = (N + S + 1) * (E + W + 1);
-    if constexpr (std::is_same_v<T, int32_t>) return static_cast<int32_t>(s / count);
-    else return s / T(count);
+    return acc_div<T>(s, kCount);
+  }
+
+  template <typename T, int K>
+  __device__ __forceinline__ void column(const T* centre, int pitch, const OpParams<T>&,
+                                         T (&res)[K]) const {
+    using A = typename Acc<T>::type;
+    A rows[K + N + S];
+#pragma unroll
+    for (int i = 0; i < K + N + S; ++i) rows[i] = row_sum<T>(centre + (i - N) * pitch);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      A s = rows[k];
+#pragma unroll
+      for (int j = 1; j <= N + S; ++j) s = acc_add2<T>(s, rows[k + j]);
+      res[k] = acc_div<T>(s, kCount);
+    }
   }
 };
 
 // ------------------------------------------------------------------ gaussian
-// Binomial blur: w(i,j) = C(2g,g+i) C(2g,g+j) / 2^(4g), row-major sum of
-// w * v (mul then add, no FMA).  int32: integer weights C*C, wrap-around
-// int64 sum, arithmetic shift right by 4g.
+// Separable binomial blur: b_j = C(2g, g+j) / 2^(2g) (exact in fp32/fp64).
+// Row pass r_i = b_{-g} v(i,-g) + ... + b_g v(i,g) west to east (mul, then
+// add), then s = b_{-g} r_{-g} + ... + b_g r_g north to south.  int32: integer
+// b_j = C(2g, g+j), wrap-around int64 sums, arithmetic shift right by 4g.
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type gauss_term(WeightT<T> w, typename Acc<T>::type x) {
+  if constexpr (std::is_same_v<T, int32_t>) return wrap_mul(w, x);
+  else return w * x;
+}
+
+template <typename T>
+__device__ __forceinline__ T gauss_result(typename Acc<T>::type s, int g) {
+  if constexpr (std::is_same_v<T, int32_t>) return static_cast<int32_t>(s >> (4 * g));
+  else return s;
+}
+
 struct Gaussian {
   template <typename T, class V>
   __device__ __forceinline__ T apply(const V& v, const OpParams<T>& p) const {
-    const int g = p.gauss_radius;
-    const int d = 2 * g + 1;
     using A = typename Acc<T>::type;
+    const int g = p.gauss_radius;
     A s = A(0);
     for (int i = -g; i <= g; ++i) {
-      for (int j = -g; j <= g; ++j) {
-        WeightT<T> w = p.gauss_w[(i + g) * d + (j + g)];
-        if constexpr (std::is_same_v<T, int32_t>) {
-          s = wrap_add(s, wrap_mul(w, (long long)v.at(i, j)));
-        } else {
-          s = s + w * v.at(i, j);
-        }
-      }
+      A row = gauss_term<T>(p.gauss_b[0], A(v.at(i, -g)));
+      for (int j = -g + 1; j <= g; ++j) row = acc_add2<T>(row, gauss_term<T>(p.gauss_b[j + g], A(v.at(i, j))));
+      const A t = gauss_term<T>(p.gauss_b[i + g], row);
+      s = i == -g ? t : acc_add2<T>(s, t);
     }
-    if constexpr (std::is_same_v<T, int32_t>) return static_cast<int32_t>(s >> (4 * g));
-    else return s;
+    return gauss_result<T>(s, g);
+  }
+};
+
+// Fixed radius (the reference kernel's default g = 5) with a column form:
+// the K + 2G row passes are shared by the K cells of a work-item.
+template <int G>
+struct GaussianFixed {
+  static constexpr bool kColumn = true;
+
+  template <typename T, class V>
+  __device__ __forceinline__ T apply(const V& v, const OpParams<T>& p) const {
+    return Gaussian{}.template apply<T>(v, p);
+  }
+
+  template <typename T, int K>
+  __device__ __forceinline__ void column(const T* centre, int pitch, const OpParams<T>& p,
+                                         T (&res)[K]) const {
+    using A = typename Acc<T>::type;
+    A rows[K + 2 * G];
+#pragma unroll
+    for (int i = 0; i < K + 2 * G; ++i) {
+      const T* r = centre + (i - G) * pitch;
+      A row = gauss_term<T>(p.gauss_b[0], A(r[-G]));
+#pragma unroll
+      for (int j = -G + 1; j <= G; ++j) row = acc_add2<T>(row, gauss_term<T>(p.gauss_b[j + G], A(r[j])));
+      rows[i] = row;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      A s = gauss_term<T>(p.gauss_b[0], rows[k]);
+#pragma unroll
+      for (int i = 1; i <= 2 * G; ++i) s = acc_add2<T>(s, gauss_term<T>(p.gauss_b[i], rows[k + i]));
+      res[k] = gauss_result<T>(s, G);
+    }
   }
 };
 

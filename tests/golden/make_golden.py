@@ -67,25 +67,28 @@ def run(op, grid, n, s, e, w, border="pad", pad=0.0, complexity=0, instructions=
                   if dr or dc)
         alive = v(0, 0) != 0
         return np.where((cnt == 3) | (alive & (cnt == 2)), 1, 0).astype(dt)
-    if op == "boxmean":
-        acc = np.zeros((H, W), np.int64 if isint else dt)
+    if op == "boxmean":  # sum of row sums (west->east), rows north->south
+        acc = None
         for dr in range(-n, s + 1):
-            for dc in range(-w, e + 1):
-                acc = acc + v(dr, dc)
+            row = v(dr, -w)
+            for dc in range(-w + 1, e + 1):
+                row = row + v(dr, dc)
+            acc = row if acc is None else acc + row
         cnt = (n + s + 1) * (e + w + 1)
         return trunc_div(acc, cnt).astype(dt) if isint else acc / f(cnt)
     if op == "gaussian":
         g = n
         from math import comb
-        acc = np.zeros((H, W), np.int64 if isint else dt)
+        # separable: row pass west->east, then the rows north->south
+        b = [comb(2 * g, g + j) for j in range(-g, g + 1)]
+        bw = [np.int64(c) if isint else f(np.ldexp(float(c), -2 * g)) for c in b]
+        acc = None
         for i in range(-g, g + 1):
-            for j in range(-g, g + 1):
-                cij = comb(2 * g, g + i) * comb(2 * g, g + j)
-                if isint:
-                    acc = acc + np.int64(cij) * v(i, j)
-                else:
-                    wgt = f(np.ldexp(float(cij), -4 * g))
-                    acc = acc + wgt * v(i, j)
+            row = bw[0] * v(i, -g)
+            for j in range(-g + 1, g + 1):
+                row = row + bw[j + g] * v(i, j)
+            t = bw[i + g] * row
+            acc = t if acc is None else acc + t
         return (acc >> (4 * g)).astype(dt) if isint else acc
     if op == "sobel":
         if isint:
@@ -153,6 +156,8 @@ CASES = [
     ("boxmean_5130_i32_pad", "boxmean", "int32", 5, 1, 3, 0, "pad", 3.0, 0, 0),
     ("gaussian_g1_f32_nearest", "gaussian", "float32", 1, 1, 1, 1, "nearest", 0.0, 0, 0),
     ("gaussian_g3_f64_pad", "gaussian", "float64", 3, 3, 3, 3, "pad", 0.0, 0, 0),
+    ("gaussian_g5_f32_nearest", "gaussian", "float32", 5, 5, 5, 5, "nearest", 0.0, 0, 0),
+    ("gaussian_g5_i32_pad", "gaussian", "int32", 5, 5, 5, 5, "pad", 0.0, 0, 0),
     ("gaussian_g2_i32_nearest", "gaussian", "int32", 2, 2, 2, 2, "nearest", 0.0, 0, 0),
     ("sobel_f32_nearest", "sobel", "float32", 1, 1, 1, 1, "nearest", 0.0, 0, 0),
     ("sobel_i32_pad", "sobel", "int32", 1, 1, 1, 1, "pad", 0.0, 0, 0),
