@@ -110,22 +110,18 @@ def traffic_for(config: str, block: str):
 
 
 # --------------------------------------------------------------------- ours
-def predict_block(config: str, W: int, H: int, dtype: str):
-    """The autotuner's prediction (wgtb predict: trained model + live device
-    probe) for this scenario, or None when no trained bundle is present."""
+def predict_block(st, config: str, W: int, H: int):
+    """The autotuner's prediction (in-process wgtb_predict: the trained bundle
+    + live device probes) for this scenario, or None without a bundle."""
+    from paper_1511_02490_b200 import autotune
+
     model = ROOT / "results" / "b200" / "model.json"
     kernel = ROOT / "results" / "b200" / "descriptors" / "kernels" / f"{'he' if config == 'heat' else config}.json"
-    wgtb = ROOT / "paper_1511_02490_b200" / "lib" / "wgtb"
-    if not (model.exists() and kernel.exists() and wgtb.exists()):
+    if not (model.exists() and kernel.exists()):
         return None, "no trained model bundle (results/b200/model.json)"
-    t = {"int32": "INT32", "float32": "FLOAT32", "float64": "FLOAT64"}[dtype]
-    proc = subprocess.run([str(wgtb), "predict", "--model", str(model), "--kernel-json", str(kernel),
-                           "--dataset", f"{W}x{H}-{t}-{t}", "--device", "cuda"],
-                          capture_output=True, text=True, timeout=300)
-    if proc.returncode != 0:
-        return None, proc.stderr.strip()[-200:]
-    wc, wr = map(int, proc.stdout.split())
-    return (wc, wr), json.loads(model.read_text()).get("technique", "?")
+    r = autotune.predict(st, W, H, kernel, model)
+    tech = json.loads(model.read_text()).get("technique", "?")
+    return (r["wc"], r["wr"]), f"{tech} ({r['probes']} live probe(s), {r['ms']:.3f} ms)"
 
 
 def quick_sweep(st, a, b, W, H):
@@ -199,7 +195,7 @@ def run_ours(args):
                           "oracle_pass_ms": round(best_ms, 5),
                           "oracle_over_worst": round(worst / best_ms, 2),
                           "sweep_s": round(time.time() - t0, 1)}
-            pred, how = predict_block(args.config, W, shard.rows, dtype)
+            pred, how = predict_block(st, args.config, W, shard.rows)
             if pred:
                 pv = b[shard.north:shard.north + shard.rows]
                 pa = a[shard.north:shard.north + shard.rows]

@@ -58,3 +58,9 @@ def test_bad_fields_rejected(field, value):
     setattr(d, field, value)
     rc = N.lib().sk_stencil_launch(ctypes.byref(d), 1, 1, 8, 8, 8, 8, 0, 0, 2, 2, None)
     assert rc == N.SK_EINVAL
+
+
+def test_wgtb_c_api_exports():
+    from paper_1511_02490_b200 import autotune
+    lib = autotune.lib()
+    assert hasattr(lib, "wgtb_predict") and hasattr(lib, "wgtb_last_error")

@@ -325,3 +325,17 @@ def test_stage_release_race_regression():
         if i % 4 == 3:
             bad += sum(int(not torch.equal(o, want)) for o in outs)
     assert bad == 0
+
+
+def test_in_process_autotuner_prediction_is_legal():
+    """wgtb_predict (the in-process daemon): the trained bundle proposes a
+    size for an unseen scenario, probed live; the size must launch and give
+    the oracle's output."""
+    from paper_1511_02490_b200 import autotune
+    root = Path(__file__).resolve().parent.parent / "results" / "b200"
+    st = Stencil(op="gol", dtype="int32")
+    r = autotune.predict(st, 3000, 2000, root / "descriptors" / "kernels" / "gol.json",
+                         root / "model.json")
+    assert r["wc"] * r["wr"] <= 1024 and r["probes"] >= 1
+    x = rand_grid("int32", (2000, 3000), 4, "gol")
+    assert_same(gpu_pass(st, x, r["wc"], r["wr"]), O.stencil(O.desc_from_stencil(st), x), "predicted")
