@@ -20,6 +20,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -625,14 +626,16 @@ struct Scratch {
   void* diff = nullptr;
   std::vector<cudaEvent_t> events;
 };
-std::map<int, Scratch> g_scratch;
+// Per (device, calling thread): the timing stream, event pool, flush buffer
+// and e2e staging buffers are never shared between threads (reentrant ABI).
+std::map<std::pair<int, std::thread::id>, Scratch> g_scratch;
 
 int scratch(Scratch** out) {
   DeviceInfo info;
   int dev = 0;
   if (int rc = current_device_info(&info, &dev)) return rc;
   std::lock_guard<std::mutex> lk(g_mu);
-  Scratch& s = g_scratch[dev];
+  Scratch& s = g_scratch[{dev, std::this_thread::get_id()}];
   if (!s.stream) {
     if (cudaStreamCreate(&s.stream) != cudaSuccess || cudaEventCreate(&s.ev0) != cudaSuccess ||
         cudaEventCreate(&s.ev1) != cudaSuccess) {
