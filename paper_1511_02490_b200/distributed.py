@@ -146,18 +146,19 @@ def iterate_sharded_overlapped(a: torch.Tensor, b: torch.Tensor, shard: RowShard
     """CUDA executor with the halo exchange hidden behind the interior.
 
     Per generation (src -> dst) on the compute stream: the boundary strips
-    (the first N and last S owned rows, the only rows that read halos) are
-    computed first; the exchange of dst's new boundary rows then runs on a
-    communication stream while the interior rows [N, rows - S), which read
-    only owned rows of src, are computed.  The next generation's boundary
-    strips wait for that exchange.  Bit-identical to iterate_sharded."""
+    are computed first.  Each strip is m = max(N, S) rows deep, because it
+    must hold both the rows that read a halo (the first N / last S owned
+    rows) and the rows the neighbour needs next (the first S rows go to p-1,
+    the last N rows to p+1).  The exchange of dst's new boundary rows then
+    runs on a communication stream while the interior rows [m, rows - m),
+    which read only owned rows of src, are computed.  The next generation's
+    boundary strips wait for that exchange.  Bit-identical to
+    iterate_sharded."""
     shard.check()
     n, s, h = shard.north, shard.south, shard.rows
-    if h < 2 * max(n, s, 1) or shard.world == 1:
+    m = max(n, s)
+    if h < 2 * max(m, 1) or shard.world == 1:
         return iterate_sharded(a, b, shard, iterations, cuda_step(stencil, wc, wr), group)
-    compute = torch.cuda.current_stream()
-    comm = torch.cuda.Stream()
-    exchanged = torch.cuda.Event()
 
     def rows(src, dst, r0, r1):
         stencil(src[n + r0:], dst[n + r0:], wc, wr,
@@ -166,16 +167,33 @@ def iterate_sharded_overlapped(a: torch.Tensor, b: torch.Tensor, shard: RowShard
 
     exchange_halos(a, shard, group)  # initial halos of the input
     src, dst = a, b
+    if not a.is_cuda:
+        # Host tensors (the multi-process CPU tests): the same schedule run
+        # serially in its worst-case order - the exchange completes before
+        # the interior is computed - so a strip that misses a row the
+        # neighbour needs shows up as a wrong halo.
+        for _ in range(iterations):
+            rows(src, dst, 0, m)
+            rows(src, dst, h - m, h)
+            exchange_halos(dst, shard, group)
+            if h - 2 * m > 0:
+                rows(src, dst, m, h - m)
+            src, dst = dst, src
+        return src
+    compute = torch.cuda.current_stream()
+    comm = torch.cuda.Stream()
+    exchanged = torch.cuda.Event()
     for _ in range(iterations):
-        rows(src, dst, 0, n)             # top strip (reads the north halo)
-        rows(src, dst, h - s, h)         # bottom strip (reads the south halo)
+        rows(src, dst, 0, m)             # top strip: reads the north halo, feeds p-1
+        rows(src, dst, h - m, h)         # bottom strip: reads the south halo, feeds p+1
         strips = torch.cuda.Event()
         strips.record(compute)
         with torch.cuda.stream(comm):
             comm.wait_event(strips)
             exchange_halos(dst, shard, group)
             exchanged.record(comm)
-        rows(src, dst, n, h - s)         # interior, concurrent with the exchange
+        if h - 2 * m > 0:
+            rows(src, dst, m, h - m)     # interior, concurrent with the exchange
         compute.wait_event(exchanged)
         src, dst = dst, src
     return src

@@ -54,6 +54,10 @@ def main():
             same = got.tobytes() == want.tobytes() and all(p[2] for p in parts)
             print(f"{op}: {'match' if same else 'MISMATCH'} (overlapped: {[p[2] for p in parts]})",
                   flush=True)
+            if not same:
+                bad = np.argwhere(got != want)
+                print(f"  {len(bad)} cells differ; rows {sorted(set(bad[:, 0].tolist()))[:12]}",
+                      flush=True)
             ok = ok and same
     if rank == 0:
         print("ALL_OK" if ok else "FAILED", flush=True)

@@ -15,7 +15,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle_lib as O
-from paper_1511_02490_b200.distributed import RowShard, iterate_sharded, scatter_rows
+from paper_1511_02490_b200.distributed import (RowShard, iterate_sharded,
+                                               iterate_sharded_overlapped, scatter_rows)
 
 CASES = {
     "gol": dict(op="gol", dtype="int32", n=1, s=1, e=1, w=1, border="pad", pad=0.0),
@@ -48,7 +49,23 @@ def oracle_step(desc):
     return step
 
 
-def worker(rank, world, port, case, q):
+class OracleStencil:
+    """The executor's call signature (Stencil.__call__) over the CPU oracle,
+    so the overlapped schedule's strip/exchange logic runs on host tensors."""
+
+    def __init__(self, desc):
+        self.desc = desc
+
+    def __call__(self, src, dst, wc, wr, rows_above=0, rows_below=0, height=None):
+        base = src.storage_offset()
+        full = src.as_strided((src.shape[0] + rows_above, src.shape[1]), src.stride(),
+                              base - rows_above * src.stride(0))
+        win = full[:rows_above + height + rows_below].numpy()
+        out = O.stencil(self.desc, win, rows_above=rows_above, rows_below=rows_below, threads=1)
+        dst[:height] = torch.from_numpy(out)
+
+
+def worker(rank, world, port, case, q, overlapped=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,7 +75,10 @@ def worker(rank, world, port, case, q):
         shard = RowShard(H, W, rank, world, c["n"], c["s"])
         a = scatter_rows(full, shard)
         b = torch.zeros_like(a)
-        res = iterate_sharded(a, b, shard, ITERS, oracle_step(oracle_desc(c)))
+        if overlapped:
+            res = iterate_sharded_overlapped(a, b, shard, ITERS, OracleStencil(oracle_desc(c)), 0, 0)
+        else:
+            res = iterate_sharded(a, b, shard, ITERS, oracle_step(oracle_desc(c)))
         q.put((rank, shard.r0, shard.owned(res).clone().numpy()))
     finally:
         dist.destroy_process_group()
@@ -70,13 +90,15 @@ def free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("overlapped", [False, True], ids=["serial", "overlapped"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_sharded_iteration_matches_single(world, case):
+def test_sharded_iteration_matches_single(world, case, overlapped):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, case, q, overlapped))
+             for r in range(world)]
     for p in procs:
         p.start()
     parts = [q.get(timeout=120) for _ in range(world)]
