@@ -76,7 +76,12 @@ typedef enum {
 typedef enum {
   SK_LOAD_AUTO = 0,     /* TMA when the tile/tensor constraints allow       */
   SK_LOAD_TMA = 1,      /* force the TMA-pipelined persistent kernel        */
-  SK_LOAD_EXPLICIT = 2  /* force explicit coalesced loads (one tile/block)  */
+  SK_LOAD_EXPLICIT = 2, /* force explicit coalesced loads (one tile/block)  */
+  SK_LOAD_BITPLANE = 3  /* gol only: bit-sliced tile (one bit per cell in
+                           shared memory, 32 cells per logic op), any number
+                           of fused generations; AUTO takes it for gol when
+                           fused_iterations >= 2.  Work-item = 32 cells of a
+                           row x K rows; tile = wc words x wr*K rows.       */
 } sk_load_path;
 
 /* Stencil descriptor: the kernel half of a reference KernelDescriptor
@@ -103,7 +108,10 @@ typedef struct {
                           then advances TB generations; sk_stencil_iterate
                           splits `iterations` into fused launches + single
                           passes.  Supported for five_point, heat, gol and
-                          boxmean on the TMA path.                            */
+                          boxmean on the TMA path.  gol on the bit-plane
+                          path (SK_LOAD_BITPLANE, or AUTO with TB >= 2)
+                          takes any TB in [1, 128]; sk_stencil_iterate then
+                          runs ceil(iterations / TB) launches.               */
 } sk_stencil_desc;
 
 /* Launch one stencil pass over a W x H region, out-of-place, on `stream`

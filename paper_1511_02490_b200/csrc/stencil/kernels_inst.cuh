@@ -2,6 +2,7 @@
 // defines the registry function SK_REGISTRY_FN (see registry.cuh).
 #include "kernels.cuh"
 #include "fused.cuh"
+#include "gol_bits.cuh"
 #include "registry.cuh"
 
 namespace sk {
@@ -40,6 +41,8 @@ KernelPtr fused_for(int K, int TB) {
 }
 
 }  // namespace
+
+KernelPtr SK_BITS_FN() { return reinterpret_cast<KernelPtr>(&k_gol_bits<SK_T>); }
 
 KernelPtr SK_FUSED_FN(const sk_stencil_desc& d, int K, int TB) {
   using T = SK_T;

@@ -24,6 +24,7 @@
 #include <tuple>
 #include <vector>
 
+#include "gol_bits.cuh"
 #include "kernels.cuh"
 #include "registry.cuh"
 #include "sk_stencil.h"
@@ -138,6 +139,16 @@ void fill_params(const sk_stencil_desc& d, OpParams<T>* p) {
 }
 
 // ------------------------------------------------------- descriptor checks
+constexpr int kMaxBitsTB = 128;
+
+// Game of Life takes the bit-plane kernel when asked to, or under AUTO once
+// generations are fused (the per-cell fused kernel stays reachable through
+// SK_LOAD_TMA for comparison).
+bool uses_bits(const sk_stencil_desc& d) {
+  return d.op == SK_OP_GOL &&
+         (d.load_path == SK_LOAD_BITPLANE || (d.load_path == SK_LOAD_AUTO && d.fused_iterations > 1));
+}
+
 int validate_desc(const sk_stencil_desc* d) {
   if (!d) return fail(SK_EINVAL, "null descriptor");
   if (d->op < 0 || d->op >= SK_OP_COUNT) return fail(SK_EINVAL, "bad op %d", d->op);
@@ -145,8 +156,11 @@ int validate_desc(const sk_stencil_desc* d) {
   if (d->border_mode != SK_BORDER_PAD && d->border_mode != SK_BORDER_NEAREST) {
     return fail(SK_EINVAL, "bad border mode %d", d->border_mode);
   }
-  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_EXPLICIT) {
+  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_BITPLANE) {
     return fail(SK_EINVAL, "bad load path %d", d->load_path);
+  }
+  if (d->load_path == SK_LOAD_BITPLANE && d->op != SK_OP_GOL) {
+    return fail(SK_ENOTSUP, "the bit-plane path is Game of Life only");
   }
   for (int b : {d->north, d->south, d->east, d->west}) {
     if (b < 0 || b > 64) return fail(SK_EINVAL, "border values must be in [0, 64]");
@@ -155,8 +169,12 @@ int validate_desc(const sk_stencil_desc* d) {
       d->cells_per_thread != 4 && d->cells_per_thread != 8) {
     return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
   }
-  if (d->fused_iterations != 0 && d->fused_iterations != 1 && d->fused_iterations != 2 &&
-      d->fused_iterations != 4) {
+  if (uses_bits(*d)) {
+    if (d->fused_iterations < 0 || d->fused_iterations > kMaxBitsTB) {
+      return fail(SK_EINVAL, "bit-plane fused_iterations must be in [0, %d]", kMaxBitsTB);
+    }
+  } else if (d->fused_iterations != 0 && d->fused_iterations != 1 && d->fused_iterations != 2 &&
+             d->fused_iterations != 4) {
     return fail(SK_EINVAL, "fused_iterations must be 0, 1, 2 or 4");
   }
   int need = 0;
@@ -593,9 +611,124 @@ int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, voi
   return SK_OK;
 }
 
+// ------------------------------------------------------- bit-plane (gol)
+KernelPtr bits_kernel(int dtype) {
+  switch (dtype) {
+    case SK_INT32: return gol_bits_i32();
+    case SK_FLOAT32: return gol_bits_f32();
+    default: return gol_bits_f64();
+  }
+}
+
+struct BitPlan {
+  BitGeom g{};
+  KernelPtr kernel = nullptr;
+  int threads = 0;      // launched (wc*wr rounded up to whole warps)
+  int smem = 0;
+  long long grid = 0;
+  int kernel_max = 0;
+  long long tile_bytes = 0;
+};
+
+// Rows per work-item: the descriptor's K, or AUTO = the power of two that
+// makes the tile about max(128, 4 TB) rows (halo overhead 2 TB / th), no
+// taller than the grid needs.
+int bits_rows_per_item(const sk_stencil_desc& d, int wr, long long H, int tb) {
+  if (d.cells_per_thread > 0) return d.cells_per_thread;
+  const long long want = std::min<long long>(std::max(128, 4 * tb), std::max<long long>(H, 1));
+  int k = 1;
+  while (k < 64 && static_cast<long long>(wr) * k < want) k *= 2;
+  return k;
+}
+
+int make_bits_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
+                   long long pitch_out, long long above, long long below, int wc, int wr, int tb,
+                   const void* out, BitPlan* plan) {
+  if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
+  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
+  if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
+  if (tb < 1 || tb > kMaxBitsTB) return fail(SK_EINVAL, "bad generation count %d", tb);
+  DeviceInfo info;
+  int dev = 0;
+  if (int rc = current_device_info(&info, &dev)) return rc;
+  plan->kernel = bits_kernel(d.dtype);
+  KernelAttr attr;
+  if (int rc = kernel_attr(dev, plan->kernel, info, &attr)) return rc;
+  plan->kernel_max = std::min(info.max_threads, attr.max_threads);
+  const long long threads = static_cast<long long>(wc) * wr;
+  if (threads > plan->kernel_max) {
+    return fail(SK_OVERSIZED, "workgroup %dx%d exceeds the effective maximum %d", wc, wr,
+                plan->kernel_max);
+  }
+  plan->threads = static_cast<int>((threads + 31) / 32 * 32);
+  const int K = bits_rows_per_item(d, wr, H, tb);
+  BitGeom& g = plan->g;
+  g.pitch_in = pitch_in;
+  g.pitch_out = pitch_out;
+  g.W = static_cast<int>(W);
+  g.H = static_cast<int>(H);
+  g.lo = -static_cast<int>(std::min<long long>(above, tb));
+  g.hi = static_cast<int>(H - 1 + std::min<long long>(below, tb));
+  g.nwords = static_cast<int>((W + 31) / 32);
+  g.tw = wc;
+  g.th = wr * K;
+  g.tb = tb;
+  g.hw = (tb + 31) / 32;
+  g.bw = g.tw + 2 * g.hw;
+  g.bh = g.th + 2 * tb;
+  g.bp = g.bw + 2;
+  const long long plane = static_cast<long long>(g.bp) * (g.bh + kBitsKS);
+  g.plane = static_cast<int>((plane + 3) / 4 * 4);  // keep plane B 16-B aligned
+  g.tiles_x = static_cast<int>((g.nwords + g.tw - 1) / g.tw);
+  g.tiles_y = static_cast<int>((H + g.th - 1) / g.th);
+  g.mode = d.border_mode;
+  double padv = d.pad_value;
+  bool pad_alive = d.dtype == SK_INT32 ? static_cast<int32_t>(padv) != 0
+                   : d.dtype == SK_FLOAT32 ? static_cast<float>(padv) != 0.0f
+                                           : padv != 0.0;
+  g.padword = pad_alive ? 0xffffffffu : 0u;
+  g.vec_store = (pitch_out % 4 == 0) && (out == nullptr || reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  plan->tile_bytes = static_cast<long long>(g.bw) * 32 * g.bh * static_cast<long long>(dtype_size(d.dtype));
+  const long long smem = 2LL * g.plane * 4;
+  if (smem > attr.max_dyn_smem) {
+    return fail(SK_REFUSED, "bit planes %lld B exceed shared memory %d B", smem, attr.max_dyn_smem);
+  }
+  plan->smem = static_cast<int>(smem);
+  if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
+    return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
+  }
+  plan->grid = static_cast<long long>(g.tiles_x) * g.tiles_y;
+  if (plan->grid >= (1LL << 31)) return fail(SK_REFUSED, "grid of %lld tiles too large", plan->grid);
+  return SK_OK;
+}
+
+int launch_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
+                long long pitch_in, long long pitch_out, long long above, long long below, int wc,
+                int wr, int tb, cudaStream_t stream) {
+  BitPlan plan;
+  if (int rc = make_bits_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, tb, out, &plan)) {
+    return rc;
+  }
+  void* args[] = {const_cast<void**>(&in), &out, &plan.g};
+  cudaError_t e = cudaLaunchKernel(plan.kernel, dim3(static_cast<unsigned>(plan.grid)),
+                                   dim3(plan.threads), args, plan.smem, stream);
+  if (e != cudaSuccess) {
+    if (is_config_error(e)) {
+      cudaGetLastError();
+      return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
+    }
+    return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  }
+  return SK_OK;
+}
+
 int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
            long long pitch_in, long long pitch_out, long long above, long long below, int wc,
            int wr, cudaStream_t stream, const sk_kernel_table* custom = nullptr) {
+  if (!custom && uses_bits(d)) {
+    return launch_bits(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr,
+                       std::max(1, d.fused_iterations), stream);
+  }
   Plan plan;
   if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan, custom)) {
     return rc;
@@ -715,6 +848,21 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
   const int TB = desc->fused_iterations > 1 ? desc->fused_iterations : 1;
   sk_stencil_desc one = *desc;
   one.fused_iterations = 0;
+  if (uses_bits(*desc)) {
+    // bit-plane gol: any generation count per launch, so the remainder is
+    // one shorter launch
+    for (int done = 0; done < iterations; ++launches) {
+      const int tb = std::min(TB, iterations - done);
+      if (int rc = launch_bits(*desc, src, dst, width, height, pitch, pitch, 0, 0, wc, wr, tb,
+                               static_cast<cudaStream_t>(stream))) {
+        return rc;
+      }
+      done += tb;
+      std::swap(src, dst);
+    }
+    if (result_in_b) *result_in_b = (launches % 2) == 1;
+    return SK_OK;
+  }
   for (int done = 0; done < iterations; ++launches) {
     // TB generations per fused launch; the remainder one pass at a time
     const bool fuse = TB > 1 && iterations - done >= TB;
@@ -733,6 +881,15 @@ int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height,
                      int32_t wr, int32_t* kernel_max, int64_t* tile_bytes, int32_t* load_path) {
   g_last_error.clear();
   if (int rc = validate_desc(desc)) return rc;
+  if (uses_bits(*desc)) {
+    BitPlan bp;
+    int rc = make_bits_plan(*desc, width, height, width, width, 0, 0, wc, wr,
+                            std::max(1, desc->fused_iterations), nullptr, &bp);
+    if (kernel_max) *kernel_max = bp.kernel_max;
+    if (tile_bytes) *tile_bytes = bp.tile_bytes;
+    if (load_path) *load_path = SK_LOAD_BITPLANE;
+    return rc;
+  }
   Plan plan;
   int rc = make_plan(*desc, width, height, width, width, 0, 0, wc, wr, nullptr, &plan);
   if (kernel_max) *kernel_max = plan.kernel_max;
@@ -745,6 +902,16 @@ int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max) {
   g_last_error.clear();
   if (int rc = validate_desc(desc)) return rc;
   if (!kernel_max) return fail(SK_EINVAL, "null output");
+  if (uses_bits(*desc)) {
+    BitPlan bp;
+    int rc = make_bits_plan(*desc, 64, 64, 64, 64, 0, 0, 2, 2, std::max(1, desc->fused_iterations),
+                            nullptr, &bp);
+    if (rc == SK_OK || rc == SK_REFUSED || rc == SK_OVERSIZED) {
+      *kernel_max = bp.kernel_max;
+      return SK_OK;
+    }
+    return rc;
+  }
   Plan plan;
   // A 2x2 block on a small grid is always within the maxima; the plan
   // carries the per-kernel maximum of the path AUTO would take.

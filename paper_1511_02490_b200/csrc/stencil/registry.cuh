@@ -25,4 +25,9 @@ KernelPtr fused_i32(const sk_stencil_desc& d, int K, int TB);
 KernelPtr fused_f32(const sk_stencil_desc& d, int K, int TB);
 KernelPtr fused_f64(const sk_stencil_desc& d, int K, int TB);
 
+// Bit-sliced temporally blocked Game of Life (gol_bits.cuh): k_gol_bits<T>.
+KernelPtr gol_bits_i32();
+KernelPtr gol_bits_f32();
+KernelPtr gol_bits_f64();
+
 }  // namespace sk

@@ -62,9 +62,10 @@ class Stencil:
     pad_value: float = 0.0
     complexity: int = 0          # synthetic kernels only
     instructions: int = 100      # synthetic kernels only
-    load_path: str = "auto"      # "auto" | "tma" | "explicit"
+    load_path: str = "auto"      # "auto" | "tma" | "explicit" | "bitplane" (gol)
     cells_per_thread: int = 0    # K cells per work-item; 0 = auto
-    fused_iterations: int = 0    # temporal blocking: generations per launch (0/1, 2, 4)
+    fused_iterations: int = 0    # temporal blocking: generations per launch
+                                 # (0/1, 2, 4; gol on the bit-plane path: 1..128)
     _desc: N.sk_stencil_desc = field(init=False, repr=False)
 
     def __post_init__(self):
@@ -77,7 +78,8 @@ class Stencil:
             pad_value=float(self.pad_value), complexity=int(self.complexity),
             instructions=int(self.instructions),
             load_path={"auto": N.SK_LOAD_AUTO, "tma": N.SK_LOAD_TMA,
-                       "explicit": N.SK_LOAD_EXPLICIT}[self.load_path],
+                       "explicit": N.SK_LOAD_EXPLICIT,
+                       "bitplane": N.SK_LOAD_BITPLANE}[self.load_path],
             cells_per_thread=int(self.cells_per_thread),
             fused_iterations=int(self.fused_iterations))
 
@@ -156,7 +158,8 @@ class Stencil:
         if rc not in (N.SK_OK, N.SK_OVERSIZED, N.SK_REFUSED):
             raise N.NativeError(rc, "sk_stencil_probe", N.last_error())
         return {"status": N.STATUS_NAMES[rc], "kernel_max": km.value, "tile_bytes": tb.value,
-                "load_path": "tma" if lp.value == N.SK_LOAD_TMA else "explicit"}
+                "load_path": {N.SK_LOAD_TMA: "tma", N.SK_LOAD_BITPLANE: "bitplane"}.get(
+                    lp.value, "explicit")}
 
     def kernel_max(self) -> int:
         km = ctypes.c_int32(0)
