@@ -3,5 +3,6 @@
 #define SK_T double
 #define SK_REGISTRY_FN kernels_f64
 #define SK_FUSED_FN fused_f64
-#define SK_BITS_FN gol_bits_f64
+#define SK_PACK_FN gol_pack_f64
+#define SK_UNPACK_FN gol_unpack_f64
 #include "kernels_inst.cuh"

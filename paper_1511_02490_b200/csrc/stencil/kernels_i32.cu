@@ -3,5 +3,7 @@
 #define SK_T int32_t
 #define SK_REGISTRY_FN kernels_i32
 #define SK_FUSED_FN fused_i32
-#define SK_BITS_FN gol_bits_i32
+#define SK_PACK_FN gol_pack_i32
+#define SK_UNPACK_FN gol_unpack_i32
+#define SK_STRIPS_HOME 1
 #include "kernels_inst.cuh"

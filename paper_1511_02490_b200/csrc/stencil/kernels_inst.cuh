@@ -42,7 +42,19 @@ KernelPtr fused_for(int K, int TB) {
 
 }  // namespace
 
-KernelPtr SK_BITS_FN() { return reinterpret_cast<KernelPtr>(&k_gol_bits<SK_T>); }
+KernelPtr SK_PACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_pack<SK_T>); }
+KernelPtr SK_UNPACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_unpack<SK_T>); }
+
+#ifdef SK_STRIPS_HOME
+KernelPtr gol_strips(int R) {
+  switch (R) {
+    case 8: return reinterpret_cast<KernelPtr>(&k_gol_strips<8>);
+    case 16: return reinterpret_cast<KernelPtr>(&k_gol_strips<16>);
+    case 32: return reinterpret_cast<KernelPtr>(&k_gol_strips<32>);
+    default: return nullptr;
+  }
+}
+#endif
 
 KernelPtr SK_FUSED_FN(const sk_stencil_desc& d, int K, int TB) {
   using T = SK_T;

@@ -165,7 +165,12 @@ int validate_desc(const sk_stencil_desc* d) {
   for (int b : {d->north, d->south, d->east, d->west}) {
     if (b < 0 || b > 64) return fail(SK_EINVAL, "border values must be in [0, 64]");
   }
-  if (d->cells_per_thread != 0 && d->cells_per_thread != 1 && d->cells_per_thread != 2 &&
+  if (uses_bits(*d)) {
+    if (d->cells_per_thread != 0 && d->cells_per_thread != 8 && d->cells_per_thread != 16 &&
+        d->cells_per_thread != 32) {
+      return fail(SK_EINVAL, "bit-plane cells_per_thread (rows per work-item) must be 0, 8, 16 or 32");
+    }
+  } else if (d->cells_per_thread != 0 && d->cells_per_thread != 1 && d->cells_per_thread != 2 &&
       d->cells_per_thread != 4 && d->cells_per_thread != 8) {
     return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
   }
@@ -612,46 +617,47 @@ int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, voi
 }
 
 // ------------------------------------------------------- bit-plane (gol)
-KernelPtr bits_kernel(int dtype) {
+KernelPtr pack_kernel(int dtype) {
   switch (dtype) {
-    case SK_INT32: return gol_bits_i32();
-    case SK_FLOAT32: return gol_bits_f32();
-    default: return gol_bits_f64();
+    case SK_INT32: return gol_pack_i32();
+    case SK_FLOAT32: return gol_pack_f32();
+    default: return gol_pack_f64();
+  }
+}
+KernelPtr unpack_kernel(int dtype) {
+  switch (dtype) {
+    case SK_INT32: return gol_unpack_i32();
+    case SK_FLOAT32: return gol_unpack_f32();
+    default: return gol_unpack_f64();
   }
 }
 
-struct BitPlan {
-  BitGeom g{};
+// Rows per lane of the strip kernel: the descriptor's K in {8, 16, 32}, or 16.
+int strip_rows(const sk_stencil_desc& d) { return d.cells_per_thread > 0 ? d.cells_per_thread : 16; }
+
+struct StripPlan {
+  StripGeom g{};
   KernelPtr kernel = nullptr;
-  int threads = 0;      // launched (wc*wr rounded up to whole warps)
+  int threads = 0;     // launched: wc*wr rounded up to whole warps
   int smem = 0;
   long long grid = 0;
   int kernel_max = 0;
   long long tile_bytes = 0;
 };
 
-// Rows per work-item: the descriptor's K, or AUTO = the power of two that
-// makes the tile about max(128, 4 TB) rows (halo overhead 2 TB / th), no
-// taller than the grid needs.
-int bits_rows_per_item(const sk_stencil_desc& d, int wr, long long H, int tb) {
-  if (d.cells_per_thread > 0) return d.cells_per_thread;
-  const long long want = std::min<long long>(std::max(128, 4 * tb), std::max<long long>(H, 1));
-  int k = 1;
-  while (k < 64 && static_cast<long long>(wr) * k < want) k *= 2;
-  return k;
-}
-
-int make_bits_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
-                   long long pitch_out, long long above, long long below, int wc, int wr, int tb,
-                   const void* out, BitPlan* plan) {
+// Legality and geometry of one k_gol_strips launch advancing `tb`
+// generations of a packed W x H grid whose readable rows are [lo, hi].
+int make_strips_plan(const sk_stencil_desc& d, long long W, long long H, long long lo,
+                     long long hi, int wc, int wr, int tb, StripPlan* plan) {
   if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
-  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
   if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
   if (tb < 1 || tb > kMaxBitsTB) return fail(SK_EINVAL, "bad generation count %d", tb);
   DeviceInfo info;
   int dev = 0;
   if (int rc = current_device_info(&info, &dev)) return rc;
-  plan->kernel = bits_kernel(d.dtype);
+  const int R = strip_rows(d);
+  plan->kernel = gol_strips(R);
+  if (!plan->kernel) return fail(SK_EINVAL, "bit-plane rows per work-item must be 8, 16 or 32");
   KernelAttr attr;
   if (int rc = kernel_attr(dev, plan->kernel, info, &attr)) return rc;
   plan->kernel_max = std::min(info.max_threads, attr.max_threads);
@@ -661,39 +667,31 @@ int make_bits_plan(const sk_stencil_desc& d, long long W, long long H, long long
                 plan->kernel_max);
   }
   plan->threads = static_cast<int>((threads + 31) / 32 * 32);
-  const int K = bits_rows_per_item(d, wr, H, tb);
-  BitGeom& g = plan->g;
-  g.pitch_in = pitch_in;
-  g.pitch_out = pitch_out;
+  const int nwarps = plan->threads / 32;
+  StripGeom& g = plan->g;
   g.W = static_cast<int>(W);
   g.H = static_cast<int>(H);
-  g.lo = -static_cast<int>(std::min<long long>(above, tb));
-  g.hi = static_cast<int>(H - 1 + std::min<long long>(below, tb));
+  g.lo = static_cast<int>(lo);
+  g.hi = static_cast<int>(hi);
   g.nwords = static_cast<int>((W + 31) / 32);
-  g.tw = wc;
-  g.th = wr * K;
   g.tb = tb;
   g.hw = (tb + 31) / 32;
-  g.bw = g.tw + 2 * g.hw;
-  g.bh = g.th + 2 * tb;
-  g.bp = g.bw + 2;
-  const long long plane = static_cast<long long>(g.bp) * (g.bh + kBitsKS);
-  g.plane = static_cast<int>((plane + 3) / 4 * 4);  // keep plane B 16-B aligned
-  g.tiles_x = static_cast<int>((g.nwords + g.tw - 1) / g.tw);
+  g.ow = 32 - 2 * g.hw;
+  g.th = nwarps * R - 2 * tb;
+  if (g.th < 1 || g.ow < 1) {
+    return fail(SK_REFUSED, "a %d-row x 32-word tile cannot hold %d halo generations", nwarps * R, tb);
+  }
+  g.tiles_x = (g.nwords + g.ow - 1) / g.ow;
   g.tiles_y = static_cast<int>((H + g.th - 1) / g.th);
   g.mode = d.border_mode;
-  double padv = d.pad_value;
-  bool pad_alive = d.dtype == SK_INT32 ? static_cast<int32_t>(padv) != 0
-                   : d.dtype == SK_FLOAT32 ? static_cast<float>(padv) != 0.0f
-                                           : padv != 0.0;
+  const double padv = d.pad_value;
+  const bool pad_alive = d.dtype == SK_INT32 ? static_cast<int32_t>(padv) != 0
+                         : d.dtype == SK_FLOAT32 ? static_cast<float>(padv) != 0.0f
+                                                 : padv != 0.0;
   g.padword = pad_alive ? 0xffffffffu : 0u;
-  g.vec_store = (pitch_out % 4 == 0) && (out == nullptr || reinterpret_cast<uintptr_t>(out) % 16 == 0);
-  plan->tile_bytes = static_cast<long long>(g.bw) * 32 * g.bh * static_cast<long long>(dtype_size(d.dtype));
-  const long long smem = 2LL * g.plane * 4;
-  if (smem > attr.max_dyn_smem) {
-    return fail(SK_REFUSED, "bit planes %lld B exceed shared memory %d B", smem, attr.max_dyn_smem);
-  }
-  plan->smem = static_cast<int>(smem);
+  plan->tile_bytes = static_cast<long long>(nwarps) * R * 32 * 4;  // bit tile in registers
+  plan->smem = (2 * nwarps * 64 + 64) * 4;
+  if (plan->smem > attr.max_dyn_smem) return fail(SK_REFUSED, "exchange area exceeds shared memory");
   if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
     return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
   }
@@ -702,22 +700,75 @@ int make_bits_plan(const sk_stencil_desc& d, long long W, long long H, long long
   return SK_OK;
 }
 
-int launch_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
-                long long pitch_in, long long pitch_out, long long above, long long below, int wc,
-                int wr, int tb, cudaStream_t stream) {
-  BitPlan plan;
-  if (int rc = make_bits_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, tb, out, &plan)) {
+int launch_checked(KernelPtr k, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
+  cudaError_t e = cudaLaunchKernel(k, grid, block, args, smem, stream);
+  if (e == cudaSuccess) return SK_OK;
+  if (is_config_error(e)) {
+    cudaGetLastError();
+    return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
+  }
+  return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+}
+
+int scratch_bits(long long words, void** p0, void** p1);  // below (per-thread scratch)
+
+// `iterations` generations of gol on the bit-plane path: pack (T -> bits,
+// rows [-above, H + below) when the generations fit one launch), then
+// ceil(iterations / TB) strip launches ping-ponging two packed grids, then
+// unpack into `out`.  Halo rows are only meaningful for a single launch
+// (iterations <= TB), as for sk_stencil_launch on a row shard.
+int run_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
+             long long pitch_in, long long pitch_out, long long above, long long below, int wc,
+             int wr, int iterations, int TB, cudaStream_t stream) {
+  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
+  TB = std::max(1, TB);
+  const long long a = iterations <= TB ? std::min<long long>(above, iterations) : 0;
+  const long long b = iterations <= TB ? std::min<long long>(below, iterations) : 0;
+  StripPlan first;
+  if (int rc = make_strips_plan(d, W, H, -a, H - 1 + b, wc, wr, std::max(1, std::min(TB, iterations)),
+                                &first)) {
     return rc;
   }
-  void* args[] = {const_cast<void**>(&in), &out, &plan.g};
-  cudaError_t e = cudaLaunchKernel(plan.kernel, dim3(static_cast<unsigned>(plan.grid)),
-                                   dim3(plan.threads), args, plan.smem, stream);
-  if (e != cudaSuccess) {
-    if (is_config_error(e)) {
-      cudaGetLastError();
-      return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
+  if (iterations == 0) return SK_OK;
+  const long long pw = (first.g.nwords + 3) / 4 * 4;  // 16-B packed rows
+  void* P[2] = {nullptr, nullptr};
+  if (int rc = scratch_bits(pw * (H + a + b), &P[0], &P[1])) return rc;
+  DeviceInfo info;
+  if (int rc = current_device_info(&info)) return rc;
+  const int cvt_grid = 4 * info.sms * 8;  // 8 warps per block, grid-stride
+  {  // pack rows [-a, H + b) of `in` into P[0]
+    const void* base = static_cast<const char*>(in) - a * pitch_in * static_cast<long long>(dtype_size(d.dtype));
+    int row0 = 0, rows = static_cast<int>(H + a + b), w = static_cast<int>(W);
+    long long pi = pitch_in, pwl = pw;
+    void* args[] = {&base, &pi, &row0, &rows, &w, &P[0], &pwl};
+    if (int rc = launch_checked(pack_kernel(d.dtype), dim3(cvt_grid), dim3(256), args, 0, stream)) return rc;
+  }
+  int cur = 0, done = 0;
+  for (bool firstl = true; done < iterations; firstl = false) {
+    const int tb = std::min(TB, iterations - done);
+    StripPlan plan;
+    if (int rc = make_strips_plan(d, W, H, firstl ? -a : 0, firstl ? H - 1 + b : H - 1, wc, wr, tb, &plan)) {
+      return rc;
     }
-    return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+    plan.g.pw_in = pw;
+    plan.g.pw_out = pw;
+    const uint32_t* src = static_cast<const uint32_t*>(P[cur]) + (firstl ? a * pw : 0);
+    uint32_t* dst = static_cast<uint32_t*>(P[1 - cur]);
+    void* args[] = {&src, &dst, &plan.g};
+    if (int rc = launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads),
+                                args, plan.smem, stream)) {
+      return rc;
+    }
+    cur = 1 - cur;
+    done += tb;
+  }
+  {  // unpack P[cur] rows [0, H) into `out`
+    const void* src = P[cur];
+    long long pwl = pw, po = pitch_out;
+    int rows = static_cast<int>(H), w = static_cast<int>(W);
+    int vec = (pitch_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    void* args[] = {&src, &pwl, &rows, &w, &out, &po, &vec};
+    if (int rc = launch_checked(unpack_kernel(d.dtype), dim3(cvt_grid), dim3(256), args, 0, stream)) return rc;
   }
   return SK_OK;
 }
@@ -726,8 +777,8 @@ int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, lon
            long long pitch_in, long long pitch_out, long long above, long long below, int wc,
            int wr, cudaStream_t stream, const sk_kernel_table* custom = nullptr) {
   if (!custom && uses_bits(d)) {
-    return launch_bits(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr,
-                       std::max(1, d.fused_iterations), stream);
+    const int tb = std::max(1, d.fused_iterations);
+    return run_bits(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr, tb, tb, stream);
   }
   Plan plan;
   if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan, custom)) {
@@ -758,6 +809,8 @@ struct Scratch {
   size_t dev_bytes = 0;
   void* diff = nullptr;
   std::vector<cudaEvent_t> events;
+  void* bits[2] = {nullptr, nullptr};  // packed bit grids of the chained gol path
+  size_t bits_bytes = 0;
 };
 // Per (device, calling thread): the timing stream, event pool, flush buffer
 // and e2e staging buffers are never shared between threads (reentrant ABI).
@@ -780,6 +833,27 @@ int scratch(Scratch** out) {
     }
   }
   *out = &s;
+  return SK_OK;
+}
+
+// Packed ping-pong grids of the bit-plane path (per device and thread, kept
+// and grown as needed; freed with the process).
+int scratch_bits(long long words, void** p0, void** p1) {
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  const size_t need = static_cast<size_t>(words) * 4;
+  if (s->bits_bytes < need) {
+    cudaFree(s->bits[0]);
+    cudaFree(s->bits[1]);
+    s->bits[0] = s->bits[1] = nullptr;
+    s->bits_bytes = 0;
+    if (cudaMalloc(&s->bits[0], need) != cudaSuccess || cudaMalloc(&s->bits[1], need) != cudaSuccess) {
+      return fail(SK_ECUDA, "bit-grid scratch allocation failed (%zu B)", need);
+    }
+    s->bits_bytes = need;
+  }
+  *p0 = s->bits[0];
+  *p1 = s->bits[1];
   return SK_OK;
 }
 
@@ -849,18 +923,13 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
   sk_stencil_desc one = *desc;
   one.fused_iterations = 0;
   if (uses_bits(*desc)) {
-    // bit-plane gol: any generation count per launch, so the remainder is
-    // one shorter launch
-    for (int done = 0; done < iterations; ++launches) {
-      const int tb = std::min(TB, iterations - done);
-      if (int rc = launch_bits(*desc, src, dst, width, height, pitch, pitch, 0, 0, wc, wr, tb,
-                               static_cast<cudaStream_t>(stream))) {
-        return rc;
-      }
-      done += tb;
-      std::swap(src, dst);
+    // Bit-plane gol: pack, ceil(iterations / TB) strip launches, unpack into
+    // d_b (d_a is left as the input).
+    if (int rc = run_bits(*desc, d_a, d_b, width, height, pitch, pitch, 0, 0, wc, wr, iterations,
+                          TB, static_cast<cudaStream_t>(stream))) {
+      return rc;
     }
-    if (result_in_b) *result_in_b = (launches % 2) == 1;
+    if (result_in_b) *result_in_b = iterations > 0;
     return SK_OK;
   }
   for (int done = 0; done < iterations; ++launches) {
@@ -882,11 +951,11 @@ int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height,
   g_last_error.clear();
   if (int rc = validate_desc(desc)) return rc;
   if (uses_bits(*desc)) {
-    BitPlan bp;
-    int rc = make_bits_plan(*desc, width, height, width, width, 0, 0, wc, wr,
-                            std::max(1, desc->fused_iterations), nullptr, &bp);
-    if (kernel_max) *kernel_max = bp.kernel_max;
-    if (tile_bytes) *tile_bytes = bp.tile_bytes;
+    StripPlan sp;
+    int rc = make_strips_plan(*desc, width, height, 0, height - 1, wc, wr,
+                              std::max(1, desc->fused_iterations), &sp);
+    if (kernel_max) *kernel_max = sp.kernel_max;
+    if (tile_bytes) *tile_bytes = sp.tile_bytes;
     if (load_path) *load_path = SK_LOAD_BITPLANE;
     return rc;
   }
@@ -903,11 +972,10 @@ int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max) {
   if (int rc = validate_desc(desc)) return rc;
   if (!kernel_max) return fail(SK_EINVAL, "null output");
   if (uses_bits(*desc)) {
-    BitPlan bp;
-    int rc = make_bits_plan(*desc, 64, 64, 64, 64, 0, 0, 2, 2, std::max(1, desc->fused_iterations),
-                            nullptr, &bp);
+    StripPlan sp;
+    int rc = make_strips_plan(*desc, 64, 64, 0, 63, 2, 2, 1, &sp);
     if (rc == SK_OK || rc == SK_REFUSED || rc == SK_OVERSIZED) {
-      *kernel_max = bp.kernel_max;
+      *kernel_max = sp.kernel_max;
       return SK_OK;
     }
     return rc;

@@ -25,9 +25,15 @@ KernelPtr fused_i32(const sk_stencil_desc& d, int K, int TB);
 KernelPtr fused_f32(const sk_stencil_desc& d, int K, int TB);
 KernelPtr fused_f64(const sk_stencil_desc& d, int K, int TB);
 
-// Bit-sliced temporally blocked Game of Life (gol_bits.cuh): k_gol_bits<T>.
-KernelPtr gol_bits_i32();
-KernelPtr gol_bits_f32();
-KernelPtr gol_bits_f64();
+// Bit-sliced temporally blocked Game of Life (gol_bits.cuh): T grid <->
+// packed bit grid conversion per element type, and the register-strip
+// generation kernel k_gol_strips<R> (R rows per lane in {8, 16, 32}).
+KernelPtr gol_pack_i32();
+KernelPtr gol_pack_f32();
+KernelPtr gol_pack_f64();
+KernelPtr gol_unpack_i32();
+KernelPtr gol_unpack_f32();
+KernelPtr gol_unpack_f64();
+KernelPtr gol_strips(int R);
 
 }  // namespace sk
