@@ -79,26 +79,45 @@ struct StripGeom {
   uint32_t padword;          // 0 or ~0
 };
 
+// Explicit 3-input logic ops (one LOP3 each; immediates for a = 0xF0,
+// b = 0xCC, c = 0xAA) so the ALU op count is exactly what is written.
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+}
+
 // Row sums of one row word c with its west/east neighbours l, r:
-// x = W + C + E as (x1 x0), y = W + E as (y1 y0).
+// x = W + C + E as (x1 x0), y = W + E as (y1 y0).  The two shifts are
+// multiplies (IMAD / IMAD.HI on the FMA pipe) because the ALU pipe, which
+// runs every LOP3, is the kernel's bound: west = c << 1 | l >> 31 =
+// c * 2 + hi(l * 2), east = c >> 1 | r << 31 = r * 2^31 + hi(c * 2^31).
 __device__ __forceinline__ void row_sums(uint32_t l, uint32_t c, uint32_t r, uint32_t& x0,
                                          uint32_t& x1, uint32_t& y0, uint32_t& y1) {
-  const uint32_t w = __funnelshift_l(l, c, 1);  // west neighbour of every bit
-  const uint32_t e = __funnelshift_r(c, r, 1);  // east neighbour
-  y0 = w ^ e;
-  y1 = w & e;
-  x0 = y0 ^ c;
-  x1 = y1 | (c & y0);
+  uint32_t w, e;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "mul.hi.u32 t, %2, 2;\n\t"
+      "mad.lo.u32 %0, %3, 2, t;\n\t"
+      "mul.hi.u32 t, %3, 0x80000000;\n\t"
+      "mad.lo.u32 %1, %4, 0x80000000, t;\n\t}"
+      : "=r"(w), "=r"(e)
+      : "r"(l), "r"(c), "r"(r));
+  x0 = lop3<0x96>(w, c, e);  // w ^ c ^ e
+  x1 = lop3<0xE8>(w, c, e);  // maj(w, c, e)
+  y0 = lop3<0x3C>(w, e, 0);  // w ^ e
+  y1 = lop3<0xC0>(w, e, 0);  // w & e
 }
 
 // next state of centre row b (alive, 2-sum y) between rows with 3-sums xa, xc
 __device__ __forceinline__ uint32_t next_state(uint32_t xa0, uint32_t xa1, uint32_t y0, uint32_t y1,
                                                uint32_t xc0, uint32_t xc1, uint32_t alive) {
-  const uint32_t l0 = xa0 ^ y0 ^ xc0;
-  const uint32_t l1 = maj3(xa0, y0, xc0);
-  const uint32_t h0 = xa1 ^ y1 ^ xc1;
-  const uint32_t h1 = maj3(xa1, y1, xc1);
-  return (l0 | alive) & (l1 ^ h0) & ~h1;
+  const uint32_t l0 = lop3<0x96>(xa0, y0, xc0);
+  const uint32_t l1 = lop3<0xE8>(xa0, y0, xc0);
+  const uint32_t h0 = lop3<0x96>(xa1, y1, xc1);
+  const uint32_t h1 = lop3<0xE8>(xa1, y1, xc1);
+  const uint32_t t = lop3<0x14>(l1, h0, h1);  // (l1 ^ h0) & ~h1
+  return lop3<0xA8>(l0, alive, t);            // (l0 | alive) & t
 }
 
 template <int R>

@@ -23,7 +23,7 @@ rows = []
 import itertools
 cfgs = [(tb, wc, wr, k) for tb in (4, 6, 8, 10, 13, 17, 20, 25, 34)
         for (wc, wr) in [(32, 1), (32, 2), (32, 4), (32, 8), (32, 16), (32, 24), (64, 8), (32, 12), (32, 6)]
-        for k in (8, 16, 32)]
+        for k in (16, 32)]
 for tb, wc, wr, k in cfgs:
     if True:
         if True:
