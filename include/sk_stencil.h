@@ -80,7 +80,8 @@ typedef enum {
   SK_LOAD_BITPLANE = 3  /* gol only: bit-sliced tile (one bit per cell in
                            shared memory, 32 cells per logic op), any number
                            of fused generations; AUTO takes it for gol when
-                           fused_iterations >= 2.  Work-item = 32 cells of a
+                           fused_iterations >= 2, except K in {1,2,4} with
+                           TB in {2,4} (per-cell fused kernel).  Work-item = 32 cells of a
                            row x K rows; tile = wc words x wr*K rows.       */
 } sk_load_path;
 

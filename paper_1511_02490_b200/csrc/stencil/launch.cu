@@ -142,11 +142,17 @@ void fill_params(const sk_stencil_desc& d, OpParams<T>* p) {
 constexpr int kMaxBitsTB = 128;
 
 // Game of Life takes the bit-plane kernel when asked to, or under AUTO once
-// generations are fused (the per-cell fused kernel stays reachable through
-// SK_LOAD_TMA for comparison).
+// generations are fused - unless the descriptor asks for a per-cell work-item
+// shape (K = 1, 2 or 4 cells) with TB = 2 or 4, which only the per-cell fused
+// kernel has (that kernel also stays reachable through SK_LOAD_TMA).
 bool uses_bits(const sk_stencil_desc& d) {
-  return d.op == SK_OP_GOL &&
-         (d.load_path == SK_LOAD_BITPLANE || (d.load_path == SK_LOAD_AUTO && d.fused_iterations > 1));
+  if (d.op != SK_OP_GOL) return false;
+  if (d.load_path == SK_LOAD_BITPLANE) return true;
+  if (d.load_path != SK_LOAD_AUTO || d.fused_iterations <= 1) return false;
+  const int k = d.cells_per_thread;
+  const bool per_cell_k = k == 1 || k == 2 || k == 4;
+  const bool per_cell_tb = d.fused_iterations == 2 || d.fused_iterations == 4;
+  return !(per_cell_k && per_cell_tb);
 }
 
 int validate_desc(const sk_stencil_desc* d) {
