@@ -391,8 +391,8 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
 TB_CANDIDATES = {
     "gol": [("bitplane", 10, 16, 32, 12), ("bitplane", 13, 16, 32, 8), ("bitplane", 10, 16, 32, 8),
             ("bitplane", 17, 16, 32, 12), ("bitplane", 10, 32, 32, 4)],
-    "heat": [("tma", 4, 0, 64, 8), ("tma", 4, 0, 128, 4), ("tma", 2, 0, 64, 8),
-             ("tma", 4, 4, 64, 8), ("tma", 2, 8, 128, 4)],
+    "heat": [("strips", 8, 16, 32, 12), ("strips", 8, 16, 32, 8), ("strips", 12, 16, 32, 12),
+             ("strips", 8, 8, 32, 16), ("tma", 4, 8, 96, 6)],
 }
 
 
@@ -449,6 +449,8 @@ def temporal_leg(args, host, tdt, wc1, wr1, iters, peak):
     g = float(H) * W * iters / (ms / 1e3) / 1e9
     es = host.itemsize
     launches = -(-iters // tb) + (2 if lp == "bitplane" else 0)
+    if lp == "tma":  # per-cell fused: floor(iters / TB) fused launches + one-pass remainder
+        launches = iters // tb + iters % tb
     out = {"value": round(g, 1), "unit": "Gcells/s", "ms_per_step": round(ms, 4),
            "path": lp, "generations_per_launch": tb, "cells_per_thread": k, "block": f"{wc}x{wr}",
            "launches_per_step": launches, "bit_exact_vs_one_pass": True,

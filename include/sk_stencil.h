@@ -77,12 +77,19 @@ typedef enum {
   SK_LOAD_AUTO = 0,     /* TMA when the tile/tensor constraints allow       */
   SK_LOAD_TMA = 1,      /* force the TMA-pipelined persistent kernel        */
   SK_LOAD_EXPLICIT = 2, /* force explicit coalesced loads (one tile/block)  */
-  SK_LOAD_BITPLANE = 3  /* gol only: bit-sliced tile (one bit per cell in
+  SK_LOAD_BITPLANE = 3, /* gol only: bit-sliced tile (one bit per cell in
                            shared memory, 32 cells per logic op), any number
                            of fused generations; AUTO takes it for gol when
                            fused_iterations >= 2, except K in {1,2,4} with
                            TB in {2,4} (per-cell fused kernel).  Work-item = 32 cells of a
                            row x K rows; tile = wc words x wr*K rows.       */
+  SK_LOAD_STRIPS = 4    /* five_point / heat with N=S=E=W=1 only: register
+                           strips, any TB in [1, 32] generations per launch;
+                           AUTO takes it for those ops when TB > 4.  Work-
+                           item = 4 cells of a row x K rows (K in {4, 8, 16},
+                           0 = 16); the block's tile is 128 columns x
+                           (wc*wr/32)*K rows, of which 4(32 - 2 ceil(TB/4))
+                           x ((wc*wr/32)*K - 2 TB) are stored.              */
 } sk_load_path;
 
 /* Stencil descriptor: the kernel half of a reference KernelDescriptor
@@ -112,7 +119,10 @@ typedef struct {
                           boxmean on the TMA path.  gol on the bit-plane
                           path (SK_LOAD_BITPLANE, or AUTO with TB >= 2)
                           takes any TB in [1, 128]; sk_stencil_iterate then
-                          runs ceil(iterations / TB) launches.               */
+                          runs ceil(iterations / TB) launches.  five_point /
+                          heat on the register-strip path (SK_LOAD_STRIPS,
+                          or AUTO with TB > 4) take any TB in [1, 32], also
+                          ceil(iterations / TB) launches.                    */
 } sk_stencil_desc;
 
 /* Launch one stencil pass over a W x H region, out-of-place, on `stream`
@@ -216,6 +226,55 @@ const char* sk_last_error(void);
 
 /* Library version string. */
 const char* sk_version(void);
+
+/* ------------------------------------------------------------------------
+ * Peer-memory halo exchange for row-sharded iterated stencils (SURVEY.md
+ * §8e, the fused variant of the per-iteration ncclSend/ncclRecv; DESIGN.md
+ * §7.1).  Each rank owns `rows` rows of a W-wide grid in two buffers A, B of
+ * N + rows + S rows (north halo, owned rows, south halo; pitch elements per
+ * row), and a control block of SK_HALO_CONTROL_BYTES zeroed device bytes.
+ * The neighbours' buffers and control blocks are mapped into this process
+ * (sk_ipc_import of handles the peers sk_ipc_export'ed, or plain pointers
+ * when the "ranks" share one process).  Zero the control blocks and barrier
+ * the ranks before the first call.
+ * ---------------------------------------------------------------------- */
+#define SK_HALO_CONTROL_BYTES 64
+
+typedef struct {
+  unsigned char handle[64]; /* cudaIpcMemHandle_t of the containing allocation */
+  int64_t offset;           /* byte offset of the exported pointer inside it   */
+} sk_ipc_handle;
+
+/* Export / import a device pointer across processes (cudaIpc*MemHandle;
+ * peer access is enabled lazily on import). */
+int sk_ipc_export(const void* d_ptr, sk_ipc_handle* out);
+int sk_ipc_import(const sk_ipc_handle* h, void** d_ptr);
+int sk_ipc_close(void* d_ptr);
+
+typedef struct {
+  void* north_a;         /* north neighbour's A / B buffers (its row 0 = its  */
+  void* north_b;         /* first north-halo row); NULL on the first rank     */
+  void* south_a;         /* south neighbour's A / B buffers; NULL on the last */
+  void* south_b;
+  void* north_control;   /* the neighbours' control blocks                    */
+  void* south_control;
+  int64_t north_rows;    /* rows owned by the north neighbour                 */
+} sk_halo_peers;
+
+/* `iterations` generations of a row shard with the halo exchange fused into
+ * the boundary-strip pass: per generation, one k_halo_strips launch (acquire
+ * the arrival flags, compute the max(N,S)-row top and bottom strips, store
+ * them locally and into the neighbours' halo rows over the peer mapping,
+ * publish the generation) and one interior launch of the tuned executor at
+ * wc x wr - all on `stream`, no host synchronisation.  `epoch` is a host
+ * counter every rank starts at 0 and passes to each call (updated in place).
+ * The result lands in d_b when *result_in_b (odd iteration counts).
+ * Replaces: the per-iteration exchange of the NCCL schedule
+ * (paper_1511_02490_b200/distributed.py) - the reference has none (§8e). */
+int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
+                            int64_t rows, int64_t pitch, int32_t iterations, int32_t wc,
+                            int32_t wr, const sk_halo_peers* peers, void* d_control,
+                            int64_t* epoch, void* stream, int32_t* result_in_b);
 
 #ifdef __cplusplus
 }

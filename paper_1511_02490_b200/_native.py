@@ -26,7 +26,7 @@ DTYPE_NAMES = {SK_INT32: "INT32", SK_FLOAT32: "FLOAT32", SK_FLOAT64: "FLOAT64"}
 DTYPE_SIZE = {SK_INT32: 4, SK_FLOAT32: 4, SK_FLOAT64: 8}
 
 SK_BORDER_PAD, SK_BORDER_NEAREST = 0, 1
-SK_LOAD_AUTO, SK_LOAD_TMA, SK_LOAD_EXPLICIT, SK_LOAD_BITPLANE = 0, 1, 2, 3
+SK_LOAD_AUTO, SK_LOAD_TMA, SK_LOAD_EXPLICIT, SK_LOAD_BITPLANE, SK_LOAD_STRIPS = 0, 1, 2, 3, 4
 
 # sk_op
 OPS = {
@@ -85,6 +85,24 @@ class NativeError(RuntimeError):
         self.code = code
 
 
+class sk_ipc_handle(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_ubyte * 64), ("offset", ctypes.c_int64)]
+
+
+class sk_halo_peers(ctypes.Structure):
+    _fields_ = [
+        ("north_a", ctypes.c_void_p),
+        ("north_b", ctypes.c_void_p),
+        ("south_a", ctypes.c_void_p),
+        ("south_b", ctypes.c_void_p),
+        ("north_control", ctypes.c_void_p),
+        ("south_control", ctypes.c_void_p),
+        ("north_rows", ctypes.c_int64),
+    ]
+
+
+SK_HALO_CONTROL_BYTES = 64
+
 _lib = None
 
 _i32, _i64, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
@@ -105,6 +123,12 @@ _PROTOTYPES = {
     "sk_device_features": (_i32, [_i32, ctypes.POINTER(sk_device_props)]),
     "sk_fill_host": (_i32, [_i32, _i32, ctypes.c_uint64, _vp, _i64]),
     "sk_buffers_equal": (_i32, [_vp, _vp, _i64, ctypes.POINTER(_i32)]),
+    "sk_ipc_export": (_i32, [_vp, ctypes.POINTER(sk_ipc_handle)]),
+    "sk_ipc_import": (_i32, [ctypes.POINTER(sk_ipc_handle), ctypes.POINTER(_vp)]),
+    "sk_ipc_close": (_i32, [_vp]),
+    "sk_stencil_iterate_peer": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32,
+                                       ctypes.POINTER(sk_halo_peers), _vp, ctypes.POINTER(_i64),
+                                       _vp, ctypes.POINTER(_i32)]),
     "sk_last_error": (ctypes.c_char_p, []),
     "sk_version": (ctypes.c_char_p, []),
 }

@@ -3,6 +3,8 @@
 #include "kernels.cuh"
 #include "fused.cuh"
 #include "gol_bits.cuh"
+#include "cross_strips.cuh"
+#include "halo.cuh"
 #include "registry.cuh"
 
 namespace sk {
@@ -40,7 +42,43 @@ KernelPtr fused_for(int K, int TB) {
   }
 }
 
+template <class Op, typename T>
+KernelPtr cross_for(int R) {
+  switch (R) {
+    case 4: return reinterpret_cast<KernelPtr>(&k_cross_strips<Op, T, 4>);
+    case 8: return reinterpret_cast<KernelPtr>(&k_cross_strips<Op, T, 8>);
+    case 16: return reinterpret_cast<KernelPtr>(&k_cross_strips<Op, T, 16>);
+    default: return nullptr;
+  }
+}
+
 }  // namespace
+
+KernelPtr SK_CROSS_FN(const sk_stencil_desc& d, int R) {
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return cross_for<FivePoint, SK_T>(R);
+    case SK_OP_HEAT: return cross_for<Heat, SK_T>(R);
+    default: return nullptr;
+  }
+}
+
+KernelPtr SK_HALO_FN(const sk_stencil_desc& d) {
+  using T = SK_T;
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return reinterpret_cast<KernelPtr>(&k_halo_strips<FivePoint, T>);
+    case SK_OP_HEAT: return reinterpret_cast<KernelPtr>(&k_halo_strips<Heat, T>);
+    case SK_OP_GOL: return reinterpret_cast<KernelPtr>(&k_halo_strips<Gol, T>);
+    case SK_OP_BOXMEAN: return reinterpret_cast<KernelPtr>(&k_halo_strips<BoxMean, T>);
+    case SK_OP_GAUSSIAN: return reinterpret_cast<KernelPtr>(&k_halo_strips<Gaussian, T>);
+    case SK_OP_SOBEL: return reinterpret_cast<KernelPtr>(&k_halo_strips<Sobel, T>);
+    case SK_OP_NMS: return reinterpret_cast<KernelPtr>(&k_halo_strips<Nms, T>);
+    case SK_OP_THRESHOLD: return reinterpret_cast<KernelPtr>(&k_halo_strips<Threshold, T>);
+    case SK_OP_SYNTHETIC: return reinterpret_cast<KernelPtr>(&k_halo_strips<Synthetic, T>);
+  }
+  return nullptr;
+}
+
+KernelPtr SK_HALO_PUT_FN() { return reinterpret_cast<KernelPtr>(&k_halo_put<SK_T>); }
 
 KernelPtr SK_PACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_pack<SK_T>); }
 KernelPtr SK_UNPACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_unpack<SK_T>); }

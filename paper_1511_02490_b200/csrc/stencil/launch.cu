@@ -24,7 +24,9 @@
 #include <tuple>
 #include <vector>
 
+#include "cross_strips.cuh"
 #include "gol_bits.cuh"
+#include "halo.cuh"
 #include "kernels.cuh"
 #include "registry.cuh"
 #include "sk_stencil.h"
@@ -155,6 +157,15 @@ bool uses_bits(const sk_stencil_desc& d) {
   return !(per_cell_k && per_cell_tb);
 }
 
+// five_point / heat with unit borders take the register-strip kernel when
+// asked to, or under AUTO for TB > 4 (beyond the per-cell fused kernel).
+constexpr int kMaxStripsTB = 32;
+bool uses_strips(const sk_stencil_desc& d) {
+  if (d.op != SK_OP_FIVE_POINT && d.op != SK_OP_HEAT) return false;
+  if (d.north != 1 || d.south != 1 || d.east != 1 || d.west != 1) return false;
+  return d.load_path == SK_LOAD_STRIPS || (d.load_path == SK_LOAD_AUTO && d.fused_iterations > 4);
+}
+
 int validate_desc(const sk_stencil_desc* d) {
   if (!d) return fail(SK_EINVAL, "null descriptor");
   if (d->op < 0 || d->op >= SK_OP_COUNT) return fail(SK_EINVAL, "bad op %d", d->op);
@@ -162,7 +173,7 @@ int validate_desc(const sk_stencil_desc* d) {
   if (d->border_mode != SK_BORDER_PAD && d->border_mode != SK_BORDER_NEAREST) {
     return fail(SK_EINVAL, "bad border mode %d", d->border_mode);
   }
-  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_BITPLANE) {
+  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_STRIPS) {
     return fail(SK_EINVAL, "bad load path %d", d->load_path);
   }
   if (d->load_path == SK_LOAD_BITPLANE && d->op != SK_OP_GOL) {
@@ -171,7 +182,18 @@ int validate_desc(const sk_stencil_desc* d) {
   for (int b : {d->north, d->south, d->east, d->west}) {
     if (b < 0 || b > 64) return fail(SK_EINVAL, "border values must be in [0, 64]");
   }
-  if (uses_bits(*d)) {
+  if (d->load_path == SK_LOAD_STRIPS && !uses_strips(*d)) {
+    return fail(SK_ENOTSUP, "the register-strip path is five_point / heat with N=S=E=W=1 only");
+  }
+  if (uses_strips(*d)) {
+    if (d->cells_per_thread != 0 && d->cells_per_thread != 4 && d->cells_per_thread != 8 &&
+        d->cells_per_thread != 16) {
+      return fail(SK_EINVAL, "register-strip cells_per_thread (rows per work-item) must be 0, 4, 8 or 16");
+    }
+    if (d->fused_iterations < 0 || d->fused_iterations > kMaxStripsTB) {
+      return fail(SK_EINVAL, "register-strip fused_iterations must be in [0, %d]", kMaxStripsTB);
+    }
+  } else if (uses_bits(*d)) {
     if (d->cells_per_thread != 0 && d->cells_per_thread != 8 && d->cells_per_thread != 16 &&
         d->cells_per_thread != 32) {
       return fail(SK_EINVAL, "bit-plane cells_per_thread (rows per work-item) must be 0, 8, 16 or 32");
@@ -180,7 +202,9 @@ int validate_desc(const sk_stencil_desc* d) {
       d->cells_per_thread != 4 && d->cells_per_thread != 8) {
     return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
   }
-  if (uses_bits(*d)) {
+  if (uses_strips(*d)) {
+    // checked above
+  } else if (uses_bits(*d)) {
     if (d->fused_iterations < 0 || d->fused_iterations > kMaxBitsTB) {
       return fail(SK_EINVAL, "bit-plane fused_iterations must be in [0, %d]", kMaxBitsTB);
     }
@@ -779,9 +803,122 @@ int run_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, l
   return SK_OK;
 }
 
+// ------------------------------------------- register strips (cross ops)
+KernelPtr cross_kernel(const sk_stencil_desc& d, int R) {
+  switch (d.dtype) {
+    case SK_INT32: return cross_strips_i32(d, R);
+    case SK_FLOAT32: return cross_strips_f32(d, R);
+    default: return cross_strips_f64(d, R);
+  }
+}
+
+// Rows per lane of the cross-strip kernel: the descriptor's K in {4, 8, 16}, or 16.
+int cross_rows(const sk_stencil_desc& d) { return d.cells_per_thread > 0 ? d.cells_per_thread : 16; }
+
+struct CrossPlan {
+  CrossGeom g{};
+  KernelPtr kernel = nullptr;
+  int threads = 0;
+  int smem = 0;
+  long long grid = 0;
+  int kernel_max = 0;
+  long long tile_bytes = 0;
+};
+
+// Legality and geometry of one k_cross_strips launch advancing `tb`
+// generations of a W x H region whose readable input rows are [lo, hi].
+int make_cross_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
+                    long long pitch_out, long long lo, long long hi, int wc, int wr, int tb,
+                    const void* in, const void* out, CrossPlan* plan) {
+  if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
+  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
+  if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
+  if (tb < 1 || tb > kMaxStripsTB) return fail(SK_EINVAL, "bad generation count %d", tb);
+  DeviceInfo info;
+  int dev = 0;
+  if (int rc = current_device_info(&info, &dev)) return rc;
+  const int R = cross_rows(d);
+  plan->kernel = cross_kernel(d, R);
+  if (!plan->kernel) return fail(SK_EINVAL, "register-strip rows per work-item must be 4, 8 or 16");
+  KernelAttr attr;
+  if (int rc = kernel_attr(dev, plan->kernel, info, &attr)) return rc;
+  plan->kernel_max = std::min(info.max_threads, attr.max_threads);
+  const long long threads = static_cast<long long>(wc) * wr;
+  if (threads > plan->kernel_max) {
+    return fail(SK_OVERSIZED, "workgroup %dx%d exceeds the effective maximum %d", wc, wr,
+                plan->kernel_max);
+  }
+  plan->threads = static_cast<int>((threads + 31) / 32 * 32);
+  const int nwarps = plan->threads / 32;
+  CrossGeom& g = plan->g;
+  g.pitch_in = pitch_in;
+  g.pitch_out = pitch_out;
+  g.W = static_cast<int>(W);
+  g.H = static_cast<int>(H);
+  g.lo = static_cast<int>(lo);
+  g.hi = static_cast<int>(hi);
+  g.tb = tb;
+  g.hl = (tb + 3) / 4;
+  g.oc = 4 * (32 - 2 * g.hl);
+  g.th = nwarps * R - 2 * tb;
+  if (g.th < 1 || g.oc < 4) {
+    return fail(SK_REFUSED, "a %d-row x 128-column tile cannot hold %d halo generations", nwarps * R, tb);
+  }
+  g.tiles_x = static_cast<int>((W + g.oc - 1) / g.oc);
+  g.tiles_y = static_cast<int>((H + g.th - 1) / g.th);
+  g.mode = d.border_mode;
+  const size_t es = dtype_size(d.dtype);
+  g.vec = (pitch_in % 4 == 0) && (pitch_out % 4 == 0) &&
+          (reinterpret_cast<uintptr_t>(in) % (4 * es) == 0) &&
+          (reinterpret_cast<uintptr_t>(out) % (4 * es) == 0);
+  plan->tile_bytes = static_cast<long long>(nwarps) * R * 128 * static_cast<long long>(es);  // in registers
+  plan->smem = static_cast<int>(2 * nwarps * 64 * 4 * es);
+  if (plan->smem > attr.max_dyn_smem) return fail(SK_REFUSED, "exchange area exceeds shared memory");
+  if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
+    return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
+  }
+  plan->grid = static_cast<long long>(g.tiles_x) * g.tiles_y;
+  if (plan->grid >= (1LL << 31)) return fail(SK_REFUSED, "grid of %lld tiles too large", plan->grid);
+  return SK_OK;
+}
+
+template <typename T>
+int launch_cross_typed(const sk_stencil_desc& d, const CrossPlan& plan, const void* in, void* out,
+                       cudaStream_t stream) {
+  OpParams<T> p;
+  fill_params<T>(d, &p);
+  T pad = static_cast<T>(d.pad_value);
+  const T* tin = static_cast<const T*>(in);
+  T* tout = static_cast<T*>(out);
+  void* args[] = {&tin, &tout, const_cast<CrossGeom*>(&plan.g), &pad, &p};
+  return launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads), args,
+                        plan.smem, stream);
+}
+
+// One k_cross_strips launch: `tb` generations from `in` (row 0 of the region,
+// `above` / `below` readable halo rows) into `out`.
+int run_cross(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
+              long long pitch_in, long long pitch_out, long long above, long long below, int wc,
+              int wr, int tb, cudaStream_t stream) {
+  CrossPlan plan;
+  if (int rc = make_cross_plan(d, W, H, pitch_in, pitch_out, -above, H - 1 + below, wc, wr, tb, in,
+                               out, &plan)) {
+    return rc;
+  }
+  switch (d.dtype) {
+    case SK_INT32: return launch_cross_typed<int32_t>(d, plan, in, out, stream);
+    case SK_FLOAT32: return launch_cross_typed<float>(d, plan, in, out, stream);
+    default: return launch_cross_typed<double>(d, plan, in, out, stream);
+  }
+}
+
 int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
            long long pitch_in, long long pitch_out, long long above, long long below, int wc,
            int wr, cudaStream_t stream, const sk_kernel_table* custom = nullptr) {
+  if (!custom && uses_strips(d)) {
+    return run_cross(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr,
+                     std::max(1, d.fused_iterations), stream);
+  }
   if (!custom && uses_bits(d)) {
     const int tb = std::max(1, d.fused_iterations);
     return run_bits(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr, tb, tb, stream);
@@ -875,6 +1012,36 @@ __global__ void k_count_diff(const uint4* __restrict__ a, const uint4* __restric
   if (local) atomicAdd(diff, local);
 }
 
+// ------------------------------------------- peer-memory halo exchange
+KernelPtr halo_kernel(const sk_stencil_desc& d) {
+  switch (d.dtype) {
+    case SK_INT32: return halo_strips_i32(d);
+    case SK_FLOAT32: return halo_strips_f32(d);
+    default: return halo_strips_f64(d);
+  }
+}
+KernelPtr halo_put_kernel(int dtype) {
+  switch (dtype) {
+    case SK_INT32: return halo_put_i32();
+    case SK_FLOAT32: return halo_put_f32();
+    default: return halo_put_f64();
+  }
+}
+
+template <typename T>
+int launch_halo_strips(const sk_stencil_desc& d, const void* src, void* dst, void* peer_n,
+                       void* peer_s, const long long* flag_n, const long long* flag_s,
+                       long long* pflag_n, long long* pflag_s, unsigned* done, const HaloGeom& g,
+                       int grid_x, cudaStream_t stream) {
+  OpParams<T> p;
+  fill_params<T>(d, &p);
+  T pad = static_cast<T>(d.pad_value);
+  void* args[] = {const_cast<void**>(&src), &dst, &peer_n, &peer_s, const_cast<long long**>(&flag_n),
+                  const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done,
+                  const_cast<HaloGeom*>(&g), &pad, &p};
+  return launch_checked(halo_kernel(d), dim3(grid_x, 2), dim3(256), args, 0, stream);
+}
+
 }  // namespace
 }  // namespace sk
 
@@ -938,6 +1105,20 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
     if (result_in_b) *result_in_b = iterations > 0;
     return SK_OK;
   }
+  if (uses_strips(*desc)) {
+    // Register strips: ceil(iterations / TB) launches, the last one shorter.
+    for (int done = 0; done < iterations; ++launches) {
+      const int tb = std::min(TB, iterations - done);
+      if (int rc = run_cross(*desc, src, dst, width, height, pitch, pitch, 0, 0, wc, wr, tb,
+                             static_cast<cudaStream_t>(stream))) {
+        return rc;
+      }
+      done += tb;
+      std::swap(src, dst);
+    }
+    if (result_in_b) *result_in_b = (launches % 2) == 1;
+    return SK_OK;
+  }
   for (int done = 0; done < iterations; ++launches) {
     // TB generations per fused launch; the remainder one pass at a time
     const bool fuse = TB > 1 && iterations - done >= TB;
@@ -956,6 +1137,15 @@ int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height,
                      int32_t wr, int32_t* kernel_max, int64_t* tile_bytes, int32_t* load_path) {
   g_last_error.clear();
   if (int rc = validate_desc(desc)) return rc;
+  if (uses_strips(*desc)) {
+    CrossPlan cp;
+    int rc = make_cross_plan(*desc, width, height, width, width, 0, height - 1, wc, wr,
+                             std::max(1, desc->fused_iterations), nullptr, nullptr, &cp);
+    if (kernel_max) *kernel_max = cp.kernel_max;
+    if (tile_bytes) *tile_bytes = cp.tile_bytes;
+    if (load_path) *load_path = SK_LOAD_STRIPS;
+    return rc;
+  }
   if (uses_bits(*desc)) {
     StripPlan sp;
     int rc = make_strips_plan(*desc, width, height, 0, height - 1, wc, wr,
@@ -977,6 +1167,15 @@ int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max) {
   g_last_error.clear();
   if (int rc = validate_desc(desc)) return rc;
   if (!kernel_max) return fail(SK_EINVAL, "null output");
+  if (uses_strips(*desc)) {
+    CrossPlan cp;
+    int rc = make_cross_plan(*desc, 64, 64, 64, 64, 0, 63, 2, 2, 1, nullptr, nullptr, &cp);
+    if (rc == SK_OK || rc == SK_REFUSED || rc == SK_OVERSIZED) {
+      *kernel_max = cp.kernel_max;
+      return SK_OK;
+    }
+    return rc;
+  }
   if (uses_bits(*desc)) {
     StripPlan sp;
     int rc = make_strips_plan(*desc, 64, 64, 0, 63, 2, 2, 1, &sp);
@@ -1146,6 +1345,174 @@ int sk_fill_host(int32_t dtype, int32_t kind, uint64_t seed, void* h_out, int64_
       default: return fail(SK_EINVAL, "bad dtype");
     }
   }
+  return SK_OK;
+}
+
+int sk_ipc_export(const void* d_ptr, sk_ipc_handle* out) {
+  g_last_error.clear();
+  if (!d_ptr || !out) return fail(SK_EINVAL, "null argument");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<GetRange>(nullptr);
+    }
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range) return fail(SK_ECUDA, "cuMemGetAddressRange unavailable");
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
+    return fail(SK_EINVAL, "pointer is not device memory");
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  static_assert(sizeof(h) <= sizeof(out->handle), "IPC handle size");
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->handle, &h, sizeof(h));
+  out->offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+  return SK_OK;
+}
+
+int sk_ipc_import(const sk_ipc_handle* h, void** d_ptr) {
+  g_last_error.clear();
+  if (!h || !d_ptr) return fail(SK_EINVAL, "null argument");
+  cudaIpcMemHandle_t mh;
+  std::memcpy(&mh, h->handle, sizeof(mh));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  *d_ptr = static_cast<char*>(base) + h->offset;
+  return SK_OK;
+}
+
+int sk_ipc_close(void* d_ptr) {
+  g_last_error.clear();
+  // cudaIpcCloseMemHandle takes the mapped base; imported pointers carry an
+  // offset, so resolve the containing mapping first.
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess ||
+      reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
+    cudaGetLastError();
+    return fail(SK_EINVAL, "pointer is not a mapped device allocation");
+  }
+  cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return SK_OK;
+}
+
+int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
+                            int64_t rows, int64_t pitch, int32_t iterations, int32_t wc,
+                            int32_t wr, const sk_halo_peers* peers, void* d_control,
+                            int64_t* epoch, void* stream, int32_t* result_in_b) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  const sk_stencil_desc& d = *desc;
+  if (!d_a || !d_b || !peers || !d_control || !epoch) return fail(SK_EINVAL, "null argument");
+  if (iterations < 0) return fail(SK_EINVAL, "negative iterations");
+  if (d.fused_iterations > 1 || uses_bits(d) || uses_strips(d)) {
+    return fail(SK_ENOTSUP, "the peer-exchange schedule runs one generation per exchange");
+  }
+  const int N = d.north, S = d.south;
+  const int m = std::max(N, S);
+  if (width < 1 || pitch < width || rows < std::max(m, 1)) {
+    return fail(SK_EINVAL, "shard of %lld rows cannot hold halos of N=%d, S=%d", (long long)rows, N, S);
+  }
+  if ((peers->north_a == nullptr) != (peers->north_b == nullptr) ||
+      (peers->north_a == nullptr) != (peers->north_control == nullptr) ||
+      (peers->south_a == nullptr) != (peers->south_b == nullptr) ||
+      (peers->south_a == nullptr) != (peers->south_control == nullptr)) {
+    return fail(SK_EINVAL, "incomplete peer mapping");
+  }
+  if (peers->north_a && peers->north_rows < std::max(m, 1)) return fail(SK_EINVAL, "bad north_rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool has_n = peers->north_a != nullptr, has_s = peers->south_a != nullptr;
+  const size_t es = dtype_size(d.dtype);
+  const long long row_bytes = pitch * static_cast<long long>(es);
+  long long* ctl = static_cast<long long*>(d_control);
+  const long long* flag_n = has_n ? ctl + 0 : nullptr;  // north halo arrivals (from p-1)
+  const long long* flag_s = has_s ? ctl + 1 : nullptr;  // south halo arrivals (from p+1)
+  unsigned* done = reinterpret_cast<unsigned*>(ctl + 2);
+  // I deliver the north neighbour's SOUTH halo (its flag 1) and the south
+  // neighbour's NORTH halo (its flag 0).
+  long long* pflag_n = has_n ? static_cast<long long*>(peers->north_control) + 1 : nullptr;
+  long long* pflag_s = has_s ? static_cast<long long*>(peers->south_control) + 0 : nullptr;
+  DeviceInfo info;
+  if (int rc = current_device_info(&info)) return rc;
+
+  HaloGeom g{};
+  g.pitch = pitch;
+  g.W = static_cast<int>(width);
+  g.h = static_cast<int>(rows);
+  g.above = has_n ? N : 0;
+  g.below = has_s ? S : 0;
+  g.m = m;
+  g.north_rows = S;
+  g.south_rows = N;
+  g.north_off = has_n ? (N + peers->north_rows) * pitch : 0;
+  g.south_off = 0;
+  g.mode = d.border_mode;
+  const long long B = *epoch;
+
+  // generation 0 halos: put the initial boundary rows, publish B + 1
+  {
+    g.wait_value = B;
+    g.signal_value = B + 1;
+    const void* src = static_cast<const char*>(d_a) + N * row_bytes;
+    void* pn = peers->north_a;
+    void* ps = peers->south_a;
+    const long long cells = static_cast<long long>(S + N) * width;
+    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((cells + 255) / 256, 4LL * info.sms)));
+    void* args[] = {const_cast<void**>(&src), &pn, &ps, const_cast<long long**>(&flag_n),
+                    const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done, &g};
+    if (int rc = launch_checked(halo_put_kernel(d.dtype), dim3(grid), dim3(256), args, 0, st)) return rc;
+  }
+  const int strip_grid = static_cast<int>(
+      std::max<long long>(1, std::min<long long>((static_cast<long long>(m) * width + 255) / 256, 2LL * info.sms)));
+  void* src = d_a;
+  void* dst = d_b;
+  for (int gen = 1; gen <= iterations; ++gen) {
+    g.wait_value = B + gen;
+    g.signal_value = B + gen + 1;
+    void* pn = has_n ? (gen & 1 ? peers->north_b : peers->north_a) : nullptr;
+    void* ps = has_s ? (gen & 1 ? peers->south_b : peers->south_a) : nullptr;
+    const void* s0 = static_cast<const char*>(src) + N * row_bytes;
+    void* d0 = static_cast<char*>(dst) + N * row_bytes;
+    if (m > 0) {
+      int rc;
+      switch (d.dtype) {
+        case SK_INT32:
+          rc = launch_halo_strips<int32_t>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
+          break;
+        case SK_FLOAT32:
+          rc = launch_halo_strips<float>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
+          break;
+        default:
+          rc = launch_halo_strips<double>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
+      }
+      if (rc) return rc;
+    }
+    // interior rows [m, rows - m) read only owned rows (m >= N, S)
+    const long long inner = rows - 2LL * m;
+    if (inner > 0) {
+      if (int rc = launch(d, static_cast<const char*>(s0) + m * row_bytes, static_cast<char*>(d0) + m * row_bytes,
+                          width, inner, pitch, pitch, N, S, wc, wr, st)) {
+        return rc;
+      }
+    }
+    std::swap(src, dst);
+  }
+  *epoch = B + iterations + 1;
+  if (result_in_b) *result_in_b = iterations % 2;
   return SK_OK;
 }
 

@@ -36,4 +36,19 @@ KernelPtr gol_unpack_f32();
 KernelPtr gol_unpack_f64();
 KernelPtr gol_strips(int R);
 
+// Register-strip temporal blocking of the 5-point cross ops (cross_strips.cuh):
+// k_cross_strips<Op, T, R>, R rows per lane in {4, 8, 16}; nullptr for other ops.
+KernelPtr cross_strips_i32(const sk_stencil_desc& d, int R);
+KernelPtr cross_strips_f32(const sk_stencil_desc& d, int R);
+KernelPtr cross_strips_f64(const sk_stencil_desc& d, int R);
+
+// Peer-memory halo exchange fused into the boundary-strip pass (halo.cuh):
+// k_halo_strips<Op, T> per op, and the row put k_halo_put<T>.
+KernelPtr halo_strips_i32(const sk_stencil_desc& d);
+KernelPtr halo_strips_f32(const sk_stencil_desc& d);
+KernelPtr halo_strips_f64(const sk_stencil_desc& d);
+KernelPtr halo_put_i32();
+KernelPtr halo_put_f32();
+KernelPtr halo_put_f64();
+
 }  // namespace sk

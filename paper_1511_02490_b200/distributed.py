@@ -20,10 +20,18 @@ Transport is torch.distributed point-to-point (NCCL over NVLink on B200,
 gloo on CPU for the multi-process tests).  The per-iteration compute is a
 callable so the same exchange logic drives the CUDA executor in production
 and the CPU oracle in tests.
+
+The peer transport (`iterate_sharded_peer`, C-ABI sk_stencil_iterate_peer)
+fuses the exchange into the boundary-strip kernel instead: the strips store
+the rows a neighbour needs straight into its halo through a peer mapping of
+its buffers (CUDA IPC over NVLink / NVSwitch) and publish an arrival flag the
+neighbour's next strip pass acquires on the device - no NCCL call and no host
+synchronisation per generation.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import ctypes
+from dataclasses import dataclass, field
 from typing import Callable
 
 import torch
@@ -204,3 +212,113 @@ def scatter_rows(full: torch.Tensor, shard: RowShard) -> torch.Tensor:
     buf = torch.zeros((shard.buffer_rows, shard.width), dtype=full.dtype, device=full.device)
     buf[shard.north:shard.north + shard.rows] = full[shard.r0:shard.r1]
     return buf
+
+
+# ------------------------------------------------------------ peer transport
+@dataclass
+class PeerLinks:
+    """What one rank needs for sk_stencil_iterate_peer: the neighbours' A/B
+    buffers and control blocks mapped into this process, this rank's own
+    control block (zeroed; the neighbours write its arrival flags) and the
+    epoch counter all ranks advance in lockstep."""
+    peers: object                      # _native.sk_halo_peers
+    control: torch.Tensor              # SK_HALO_CONTROL_BYTES of device memory
+    epoch: int = 0
+    imported: list = field(default_factory=list)  # IPC mappings to close
+
+    def close(self) -> None:
+        from . import _native as N
+
+        for ptr in self.imported:
+            N.lib().sk_ipc_close(ptr)
+        self.imported.clear()
+
+
+def new_control(device=None) -> torch.Tensor:
+    from . import _native as N
+
+    return torch.zeros(N.SK_HALO_CONTROL_BYTES // 8, dtype=torch.int64,
+                       device=device or torch.device("cuda"))
+
+
+def local_links(bufs: list, shards: list) -> list:
+    """Links for P "ranks" that live in one process (one stream each): the
+    neighbours' tensors are addressed directly.  bufs[p] = (a, b, control)."""
+    from . import _native as N
+
+    links = []
+    for p, sh in enumerate(shards):
+        peers = N.sk_halo_peers()
+        if p > 0:
+            a, b, c = bufs[p - 1]
+            peers.north_a, peers.north_b, peers.north_control = a.data_ptr(), b.data_ptr(), c.data_ptr()
+            peers.north_rows = shards[p - 1].rows
+        if p < len(shards) - 1:
+            a, b, c = bufs[p + 1]
+            peers.south_a, peers.south_b, peers.south_control = a.data_ptr(), b.data_ptr(), c.data_ptr()
+        links.append(PeerLinks(peers, bufs[p][2]))
+    return links
+
+
+def connect_peers(a: torch.Tensor, b: torch.Tensor, control: torch.Tensor, shard: RowShard,
+                  group=None) -> PeerLinks:
+    """Multi-process links: every rank exports IPC handles of its A, B and
+    control block, all-gathers them (any backend), and maps its neighbours'.
+    The control blocks are zero before the barrier that ends this call."""
+    from . import _native as N
+
+    torch.cuda.synchronize()
+
+    def export(t):
+        h = N.sk_ipc_handle()
+        N.check(N.lib().sk_ipc_export(t.data_ptr(), ctypes.byref(h)), "sk_ipc_export")
+        return bytes(h.handle), int(h.offset)
+
+    mine = {"a": export(a), "b": export(b), "c": export(control), "rows": shard.rows}
+    every = [None] * shard.world
+    dist.all_gather_object(every, mine, group=group)
+
+    links = PeerLinks(N.sk_halo_peers(), control)
+
+    def imp(entry):
+        h = N.sk_ipc_handle()
+        ctypes.memmove(h.handle, entry[0], len(entry[0]))
+        h.offset = entry[1]
+        ptr = ctypes.c_void_p()
+        N.check(N.lib().sk_ipc_import(ctypes.byref(h), ctypes.byref(ptr)), "sk_ipc_import")
+        links.imported.append(ptr.value)
+        return ptr.value
+
+    if shard.rank > 0:
+        e = every[shard.rank - 1]
+        links.peers.north_a, links.peers.north_b = imp(e["a"]), imp(e["b"])
+        links.peers.north_control = imp(e["c"])
+        links.peers.north_rows = e["rows"]
+    if shard.rank < shard.world - 1:
+        e = every[shard.rank + 1]
+        links.peers.south_a, links.peers.south_b = imp(e["a"]), imp(e["b"])
+        links.peers.south_control = imp(e["c"])
+    dist.barrier(group=group)
+    return links
+
+
+def iterate_sharded_peer(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iterations: int,
+                         stencil, wc: int, wr: int, links: PeerLinks, stream=None) -> torch.Tensor:
+    """`iterations` generations with the halo exchange fused into the
+    boundary-strip kernel (sk_stencil_iterate_peer).  `a` / `b` are the
+    shard's N + rows + S row buffers; returns the one holding the result.
+    Bit-identical to iterate_sharded."""
+    from . import _native as N
+
+    shard.check()
+    s = (stream or torch.cuda.current_stream(a.device)).cuda_stream
+    epoch = ctypes.c_int64(links.epoch)
+    in_b = ctypes.c_int32(0)
+    rc = N.lib().sk_stencil_iterate_peer(ctypes.byref(stencil.desc), a.data_ptr(), b.data_ptr(),
+                                         shard.width, shard.rows, a.stride(0), iterations, wc, wr,
+                                         ctypes.byref(links.peers), links.control.data_ptr(),
+                                         ctypes.byref(epoch), s or None, ctypes.byref(in_b))
+    if rc:
+        stencil._raise(rc, "sk_stencil_iterate_peer", wc, wr)
+    links.epoch = epoch.value
+    return b if in_b.value else a

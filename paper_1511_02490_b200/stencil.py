@@ -63,9 +63,11 @@ class Stencil:
     complexity: int = 0          # synthetic kernels only
     instructions: int = 100      # synthetic kernels only
     load_path: str = "auto"      # "auto" | "tma" | "explicit" | "bitplane" (gol)
+                                 # | "strips" (five_point / heat, unit borders)
     cells_per_thread: int = 0    # K cells per work-item; 0 = auto
     fused_iterations: int = 0    # temporal blocking: generations per launch
-                                 # (0/1, 2, 4; gol on the bit-plane path: 1..128)
+                                 # (0/1, 2, 4; gol on the bit-plane path: 1..128;
+                                 # five_point / heat on the strip path: 1..32)
     _desc: N.sk_stencil_desc = field(init=False, repr=False)
 
     def __post_init__(self):
@@ -79,7 +81,8 @@ class Stencil:
             instructions=int(self.instructions),
             load_path={"auto": N.SK_LOAD_AUTO, "tma": N.SK_LOAD_TMA,
                        "explicit": N.SK_LOAD_EXPLICIT,
-                       "bitplane": N.SK_LOAD_BITPLANE}[self.load_path],
+                       "bitplane": N.SK_LOAD_BITPLANE,
+                       "strips": N.SK_LOAD_STRIPS}[self.load_path],
             cells_per_thread=int(self.cells_per_thread),
             fused_iterations=int(self.fused_iterations))
 
@@ -158,7 +161,8 @@ class Stencil:
         if rc not in (N.SK_OK, N.SK_OVERSIZED, N.SK_REFUSED):
             raise N.NativeError(rc, "sk_stencil_probe", N.last_error())
         return {"status": N.STATUS_NAMES[rc], "kernel_max": km.value, "tile_bytes": tb.value,
-                "load_path": {N.SK_LOAD_TMA: "tma", N.SK_LOAD_BITPLANE: "bitplane"}.get(
+                "load_path": {N.SK_LOAD_TMA: "tma", N.SK_LOAD_BITPLANE: "bitplane",
+                              N.SK_LOAD_STRIPS: "strips"}.get(
                     lp.value, "explicit")}
 
     def kernel_max(self) -> int:
