@@ -238,8 +238,15 @@ def run_ours(args):
 
     step_fn = cuda_step(st, wc, wr)
     stream = torch.cuda.current_stream()
+    links = None
+    if world > 1 and args.transport == "peer":
+        from paper_1511_02490_b200.distributed import connect_peers, iterate_sharded_peer, new_control
+
+        links = connect_peers(a, b, new_control(), shard)
 
     def one_step():
+        if links is not None:
+            return iterate_sharded_peer(a, b, shard, iters, st, wc, wr, links)
         if world > 1 and not args.no_overlap:
             return iterate_sharded_overlapped(a, b, shard, iters, st, wc, wr)
         return iterate_sharded(a, b, shard, iters, step_fn)
@@ -267,6 +274,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     launches = args.steps * iters
+    if world > 1:  # boundary strips + interior per generation (+ the initial put: peer)
+        launches = args.steps * (2 * iters + (1 if links is not None else 0))
     cells_total = float(H) * W * iters * args.steps
     gcells = cells_total / (ms / 1e3) / 1e9
     peak, peak_kind = measured_hbm_peak()
@@ -311,7 +320,9 @@ def run_ours(args):
                 "iterations_per_step": iters,
                 "block": block,
                 "l2": f"inputs larger than L2 ({shard.rows * W * es / 1e6:.0f} MB per buffer)",
-                "parallelism": f"row-shard x{world}" + (" + NCCL halo exchange" if world > 1 else ""),
+                "parallelism": f"row-shard x{world}" + (
+                    (" + peer-memory halo exchange fused into the strip kernel"
+                     if args.transport == "peer" else " + NCCL halo exchange") if world > 1 else ""),
             },
             "hbm_frac": round(achieved / peak, 4),
             "predicted_over_oracle": sweep_info.get("predicted_over_oracle"),
@@ -458,6 +469,12 @@ def temporal_leg(args, host, tdt, wc1, wr1, iters, peak):
            "note": "the one-pass roofline does not bound this path: HBM is touched "
                    + ("once per step (pack/unpack); the packed grids (W*H/8 B) stay in L2"
                       if lp == "bitplane" else f"once per {tb} generations")}
+    prof = ROOT / "profiles" / "temporal_kernels.json"
+    if prof.exists():
+        try:
+            out["dominant_kernel_ncu"] = json.loads(prof.read_text()).get(args.config)
+        except Exception:
+            pass
     return out
 
 
@@ -560,6 +577,9 @@ def main():
                     help="skip the temporally blocked leg (TB generations per launch)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange halos between passes instead of behind the interior")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N>1 halo exchange: peer stores from the strip kernel (CUDA IPC over "
+                         "NVLink) or NCCL send/recv behind the interior")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="halo transport; gloo (host-staged) only to test the multi-rank path on 1 GPU")
     args = ap.parse_args()

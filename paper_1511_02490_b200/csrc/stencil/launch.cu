@@ -1463,6 +1463,23 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
   g.mode = d.border_mode;
   const long long B = *epoch;
 
+  // Resolve every kernel of the schedule before the first launch.  With CUDA
+  // lazy loading, loading a module may wait for the context's running
+  // kernels; a strip pass spinning on a peer whose launches this thread has
+  // not issued yet (ranks sharing one process) would then never finish.
+  {
+    int dev = 0;
+    if (int rc = current_device_info(&info, &dev)) return rc;
+    KernelAttr ka;
+    if (int rc = kernel_attr(dev, halo_kernel(d), info, &ka)) return rc;
+    if (int rc = kernel_attr(dev, halo_put_kernel(d.dtype), info, &ka)) return rc;
+    if (rows - 2LL * m > 0) {
+      Plan plan;
+      const char* a0 = static_cast<const char*>(d_a) + (N + m) * row_bytes;
+      if (int rc = make_plan(d, width, rows - 2LL * m, pitch, pitch, N, S, wc, wr, a0, &plan)) return rc;
+    }
+  }
+
   // generation 0 halos: put the initial boundary rows, publish B + 1
   {
     g.wait_value = B;

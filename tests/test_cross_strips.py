@@ -79,10 +79,10 @@ def test_strips_generation_counts(dtype, tb):
     x = grid(dtype, (300, 520), seed=tb)
     for border in ("pad", "nearest"):
         st = strips("heat", dtype, tb, 16, border)
-        if not tile_fits(min(tb, 50), 32, 16, 16):
-            assert st.probe(520, 300, 32, 16)["status"] == "REFUSED"
+        if not tile_fits(min(tb, 50), 32, 12, 16):
+            assert st.probe(520, 300, 32, 12)["status"] == "REFUSED"
             continue
-        got = run(st, x, 50, 32, 16)
+        got = run(st, x, 50, 32, 12)
         assert got.tobytes() == oracle(st, x, 50).tobytes(), f"tb={tb} {border}"
 
 

@@ -26,11 +26,15 @@ def test_sharded_cuda_iteration_matches_oracle(n):
     assert "ALL_OK" in proc.stdout, proc.stdout + proc.stderr[-3000:]
 
 
-def test_bench_two_ranks_json_line():
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_bench_two_ranks_json_line(transport):
+    """transport=peer: IPC-mapped peer stores from the strip kernel;
+    transport=nccl: the send/recv schedule (host-staged under gloo here)."""
     proc = torchrun(2, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3", "--wc", "32",
-                    "--wr", "8", "--no-cpu", "--backend", "gloo")
+                    "--wr", "8", "--no-cpu", "--backend", "gloo", "--transport", transport)
     lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
     assert proc.returncode == 0 and len(lines) == 1, proc.stdout + proc.stderr[-3000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_grid"] == "8192x16384"
     assert d["e2e"]["value"] > 0
+    assert ("peer-memory" in d["config"]["parallelism"]) == (transport == "peer")
