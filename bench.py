@@ -402,8 +402,8 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
 TB_CANDIDATES = {
     "gol": [("bitplane", 10, 16, 32, 12), ("bitplane", 13, 16, 32, 8), ("bitplane", 10, 16, 32, 8),
             ("bitplane", 17, 16, 32, 12), ("bitplane", 10, 32, 32, 4)],
-    "heat": [("strips", 8, 16, 32, 12), ("strips", 8, 16, 32, 8), ("strips", 12, 16, 32, 12),
-             ("strips", 8, 8, 32, 16), ("tma", 4, 8, 96, 6)],
+    "heat": [("strips", 8, 8, 32, 12), ("strips", 6, 8, 32, 12), ("strips", 10, 8, 32, 12),
+             ("strips", 8, 8, 32, 8), ("strips", 12, 16, 32, 12)],
 }
 
 

@@ -87,7 +87,7 @@ typedef enum {
                            strips, any TB in [1, 32] generations per launch;
                            AUTO takes it for those ops when TB > 4.  Work-
                            item = 4 cells of a row x K rows (K in {4, 8, 16},
-                           0 = 16); the block's tile is 128 columns x
+                           0 = 8, float64 4); the block's tile is 128 columns x
                            (wc*wr/32)*K rows, of which 4(32 - 2 ceil(TB/4))
                            x ((wc*wr/32)*K - 2 TB) are stored.              */
 } sk_load_path;
@@ -268,7 +268,9 @@ typedef struct {
  * publish the generation) and one interior launch of the tuned executor at
  * wc x wr - all on `stream`, no host synchronisation.  `epoch` is a host
  * counter every rank starts at 0 and passes to each call (updated in place).
- * The result lands in d_b when *result_in_b (odd iteration counts).
+ * The result lands in d_b when *result_in_b (odd iteration counts).  The
+ * peers' *_a / *_b must be the neighbours' buffers in the roles d_a / d_b
+ * play in this call (ranks ping-pong in lockstep: swap them together).
  * Replaces: the per-iteration exchange of the NCCL schedule
  * (paper_1511_02490_b200/distributed.py) - the reference has none (§8e). */
 int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,

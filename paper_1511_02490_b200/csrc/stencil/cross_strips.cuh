@@ -194,8 +194,16 @@ __device__ __forceinline__ void cross_generations(T (&v)[R][4], Quad<T>* xchg, i
 
 // Register budget per thread bounds the block (the per-kernel maximum
 // workgroup size): R x 4 state values plus the rolling rows.
+// R = 8 asks for two resident 384-thread blocks per SM (<= 80 registers):
+// with one, the SM idles on every block's tile load (ncu: long_scoreboard).
+template <int R>
+struct CrossBounds {
+  static constexpr int kThreads = R <= 4 ? 1024 : 384;
+  static constexpr int kMinBlocks = R == 8 ? 2 : 1;
+};
+
 template <class Op, typename T, int R>
-__global__ void __launch_bounds__(R <= 4 ? 1024 : (R <= 8 ? 512 : 384))
+__global__ void __launch_bounds__(CrossBounds<R>::kThreads, CrossBounds<R>::kMinBlocks)
     k_cross_strips(const T* __restrict__ in, T* __restrict__ out, const CrossGeom g, const T pad,
                    const __grid_constant__ OpParams<T> p) {
   extern __shared__ __align__(16) unsigned char sm_raw[];

@@ -812,8 +812,11 @@ KernelPtr cross_kernel(const sk_stencil_desc& d, int R) {
   }
 }
 
-// Rows per lane of the cross-strip kernel: the descriptor's K in {4, 8, 16}, or 16.
-int cross_rows(const sk_stencil_desc& d) { return d.cells_per_thread > 0 ? d.cells_per_thread : 16; }
+// Rows per lane of the cross-strip kernel: the descriptor's K in {4, 8, 16},
+// or 8 (4 for float64, whose 8-row strips spill) - two resident blocks per SM.
+int cross_rows(const sk_stencil_desc& d) {
+  return d.cells_per_thread > 0 ? d.cells_per_thread : (d.dtype == SK_FLOAT64 ? 4 : 8);
+}
 
 struct CrossPlan {
   CrossGeom g{};

@@ -223,8 +223,24 @@ class PeerLinks:
     epoch counter all ranks advance in lockstep."""
     peers: object                      # _native.sk_halo_peers
     control: torch.Tensor              # SK_HALO_CONTROL_BYTES of device memory
+    own: tuple = (0, 0)                # this rank's (A, B) data pointers as registered
     epoch: int = 0
     imported: list = field(default_factory=list)  # IPC mappings to close
+
+    def peers_for(self, a: torch.Tensor, b: torch.Tensor):
+        """The peer struct for a call on (a, b): every rank ping-pongs in
+        lockstep, so when this rank passes its buffers swapped (an odd
+        iteration count left the result in B) so do its neighbours."""
+        from . import _native as N
+
+        pa, pb = a.data_ptr(), b.data_ptr()
+        if (pa, pb) == self.own:
+            return self.peers
+        if (pb, pa) != self.own:
+            raise ValueError("iterate_sharded_peer: a/b are not the buffers the links were made for")
+        q = self.peers
+        return N.sk_halo_peers(q.north_b, q.north_a, q.south_b, q.south_a, q.north_control,
+                               q.south_control, q.north_rows)
 
     def close(self) -> None:
         from . import _native as N
@@ -256,7 +272,7 @@ def local_links(bufs: list, shards: list) -> list:
         if p < len(shards) - 1:
             a, b, c = bufs[p + 1]
             peers.south_a, peers.south_b, peers.south_control = a.data_ptr(), b.data_ptr(), c.data_ptr()
-        links.append(PeerLinks(peers, bufs[p][2]))
+        links.append(PeerLinks(peers, bufs[p][2], (bufs[p][0].data_ptr(), bufs[p][1].data_ptr())))
     return links
 
 
@@ -278,7 +294,7 @@ def connect_peers(a: torch.Tensor, b: torch.Tensor, control: torch.Tensor, shard
     every = [None] * shard.world
     dist.all_gather_object(every, mine, group=group)
 
-    links = PeerLinks(N.sk_halo_peers(), control)
+    links = PeerLinks(N.sk_halo_peers(), control, (a.data_ptr(), b.data_ptr()))
 
     def imp(entry):
         h = N.sk_ipc_handle()
@@ -314,9 +330,10 @@ def iterate_sharded_peer(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iter
     s = (stream or torch.cuda.current_stream(a.device)).cuda_stream
     epoch = ctypes.c_int64(links.epoch)
     in_b = ctypes.c_int32(0)
+    peers = links.peers_for(a, b)
     rc = N.lib().sk_stencil_iterate_peer(ctypes.byref(stencil.desc), a.data_ptr(), b.data_ptr(),
                                          shard.width, shard.rows, a.stride(0), iterations, wc, wr,
-                                         ctypes.byref(links.peers), links.control.data_ptr(),
+                                         ctypes.byref(peers), links.control.data_ptr(),
                                          ctypes.byref(epoch), s or None, ctypes.byref(in_b))
     if rc:
         stencil._raise(rc, "sk_stencil_iterate_peer", wc, wr)

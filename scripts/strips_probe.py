@@ -1,7 +1,7 @@
 """Gcells/s of heat / five_point on the register-strip path over (TB, K, wc,
 wr) on a side^2 grid, `iters` generations, CUDA events, inputs larger than L2;
 each configuration is checked bit-exact against the one-pass executor.
-usage: python scripts/strips_probe.py [op] [dtype] [side] [iters]"""
+usage: python scripts/strips_probe.py [op] [dtype] [side] [iters] [tb,tb,...]"""
 import sys
 from pathlib import Path
 
@@ -22,8 +22,9 @@ a0 = torch.from_numpy(host).cuda()
 one = Stencil(op=op, dtype=dtype, border="nearest")
 want = one.iterate(a0.clone(), torch.empty_like(a0), iters, 64, 8).clone()
 rows = []
-for tb in (4, 6, 8, 10, 12, 16):
-    for k in (8, 16):
+TBS = [int(t) for t in sys.argv[5].split(",")] if len(sys.argv) > 5 else [4, 6, 8, 10, 12, 16]
+for tb in TBS:
+    for k in (4, 8, 16):
         for wc, wr in [(32, 4), (32, 6), (32, 8), (32, 12), (32, 16), (32, 24), (64, 8), (32, 32)]:
             st = Stencil(op=op, dtype=dtype, border="nearest", load_path="strips",
                          fused_iterations=tb, cells_per_thread=k)

@@ -32,10 +32,10 @@ def strips(op, dtype, tb, k=0, border="nearest", pad=0.0):
                    fused_iterations=tb, cells_per_thread=k)
 
 
-def tile_fits(tb, wc, wr, k):
-    """ceil(wc*wr/32) warps x R rows (R = k or 16) must hold 2*TB halo rows
-    plus one output row."""
-    return ((wc * wr + 31) // 32) * (k or 16) > 2 * tb
+def tile_fits(tb, wc, wr, k, dtype="float32"):
+    """ceil(wc*wr/32) warps x R rows (R = k, or 8 / 4 for float64) must hold
+    2*TB halo rows plus one output row."""
+    return ((wc * wr + 31) // 32) * (k or (4 if dtype == "float64" else 8)) > 2 * tb
 
 
 def run(st, x, iters, wc, wr, pitch_pad=0):
@@ -66,7 +66,7 @@ def test_strips_vs_oracle(op, dtype, border, pad, shape, k):
                               (12, 12, 32, 16), (7, 3, 3, 5)]:
         st = strips(op, dtype, tb, k, border, pad)
         if st.probe(shape[1], shape[0], wc, wr)["status"] != "OK":
-            assert not tile_fits(min(tb, iters), wc, wr, k) or wc * wr > st.kernel_max()
+            assert not tile_fits(min(tb, iters), wc, wr, k, dtype) or wc * wr > st.kernel_max()
             continue
         got = run(st, x, iters, wc, wr)
         want = oracle(st, x, iters)
@@ -157,7 +157,7 @@ def test_strips_auto_and_legality():
         4096, 4096, 32, 8)["load_path"] == "tma"  # TB <= 4: the per-cell fused kernel
     st = strips("heat", "float32", 8)
     km = st.kernel_max()
-    assert km < 1024  # register-bound per-kernel maximum (R = 16 rows per lane)
+    assert km < 1024  # register-bound per-kernel maximum (R = 8 rows per lane: 384)
     assert st.probe(4096, 4096, 32, 32)["status"] == "OVERSIZED"
     # 1 warp x 4 rows cannot hold 2 x 8 halo rows
     assert strips("heat", "float32", 8, 4).probe(4096, 4096, 32, 1)["status"] == "REFUSED"
@@ -167,3 +167,18 @@ def test_strips_auto_and_legality():
         Stencil(op="heat", dtype="float32", north=2, load_path="strips").probe(64, 64, 32, 8)
     with pytest.raises(Exception):
         strips("heat", "float32", 33).probe(64, 64, 32, 8)
+
+
+@pytest.mark.parametrize("op", ["heat", "five_point"])
+def test_strips_subnormals_and_signed_zeros(op):
+    """The fp32 pair path (packed FADD2 + scalar products) must round exactly
+    like the scalar executor on subnormal inputs, signed zeros and large
+    magnitudes as well."""
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal((70, 260)) * 1e-39).astype(np.float32)  # subnormal range
+    x[::7] = -0.0
+    x[3::11] = rng.standard_normal(x[3::11].shape).astype(np.float32) * 1e30
+    for border, pad in (("nearest", 0.0), ("pad", -0.0)):
+        st = strips(op, "float32", 5, 8, border, pad)
+        got = run(st, x, 11, 32, 8)
+        assert got.tobytes() == oracle(st, x, 11).tobytes(), border
