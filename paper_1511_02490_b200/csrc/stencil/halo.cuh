@@ -165,4 +165,14 @@ __global__ void __launch_bounds__(256)
   halo_release(done, peer_flag_n, peer_flag_s, g.signal_value);
 }
 
+// Stream-ordered acquire of this rank's arrival flags (the temporally
+// blocked schedule waits here before its strip pass, whose kernel is the
+// register-strip one).
+// (A template so the header can be included by every translation unit.)
+template <int Unused = 0>
+__global__ void __launch_bounds__(32) k_halo_wait(const long long* flag_n, const long long* flag_s,
+                                                  long long value) {
+  halo_acquire(flag_n, flag_s, value);
+}
+
 }  // namespace sk

@@ -84,6 +84,8 @@ KernelPtr SK_PACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_pack<SK_T>); 
 KernelPtr SK_UNPACK_FN() { return reinterpret_cast<KernelPtr>(&k_gol_unpack<SK_T>); }
 
 #ifdef SK_STRIPS_HOME
+KernelPtr halo_wait() { return reinterpret_cast<KernelPtr>(&k_halo_wait<0>); }
+
 KernelPtr gol_strips(int R) {
   switch (R) {
     case 8: return reinterpret_cast<KernelPtr>(&k_gol_strips<8>);

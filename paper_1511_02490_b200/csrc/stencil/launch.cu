@@ -1045,6 +1045,123 @@ int launch_halo_strips(const sk_stencil_desc& d, const void* src, void* dst, voi
   return launch_checked(halo_kernel(d), dim3(grid_x, 2), dim3(256), args, 0, stream);
 }
 
+// Temporally blocked peer schedule (register-strip path, TB generations per
+// exchange).  The shard buffers carry TB-deep halos: TB*N rows above, TB*S
+// below.  Per launch k (generations (k-1)TB+1 .. kTB, the last one shorter):
+//   k_halo_wait   acquire the neighbours' state-(k-1) halos (value B + k);
+//   strips        k_cross_strips over the top / bottom m = TB*max(N,S) rows;
+//   k_halo_put    their first TB*S / last TB*N rows into the neighbours' halos,
+//                 publish B + k + 1 (last block, release.sys);
+//   interior      k_cross_strips over rows [m, rows - m), owned rows only.
+// Same one-flag-per-direction argument as the one-generation schedule: the
+// neighbour publishes state k only after its launch-k strip pass - the last
+// reader of the halo rows overwritten by launch k+1's put - has run.
+int iterate_peer_strips(const sk_stencil_desc& d, void* d_a, void* d_b, int64_t width, int64_t rows,
+                        int64_t pitch, int32_t iterations, int32_t wc, int32_t wr,
+                        const sk_halo_peers& peers, void* d_control, int64_t* epoch,
+                        cudaStream_t st, int32_t* result_in_b) {
+  const int TB = d.fused_iterations;
+  const int Nh = TB * d.north, Sh = TB * d.south;
+  const int m = std::max(Nh, Sh);
+  if (width < 1 || pitch < width || rows < 2LL * m + std::max(Nh, Sh)) {
+    return fail(SK_EINVAL, "shard of %lld rows cannot hold %d-generation strips of %d rows",
+                (long long)rows, TB, m);
+  }
+  if ((peers.north_a == nullptr) != (peers.north_b == nullptr) ||
+      (peers.north_a == nullptr) != (peers.north_control == nullptr) ||
+      (peers.south_a == nullptr) != (peers.south_b == nullptr) ||
+      (peers.south_a == nullptr) != (peers.south_control == nullptr)) {
+    return fail(SK_EINVAL, "incomplete peer mapping");
+  }
+  const bool has_n = peers.north_a != nullptr, has_s = peers.south_a != nullptr;
+  if (has_n && peers.north_rows < 2LL * m) return fail(SK_EINVAL, "bad north_rows");
+  const size_t es = dtype_size(d.dtype);
+  const long long row_bytes = pitch * static_cast<long long>(es);
+  long long* ctl = static_cast<long long*>(d_control);
+  const long long* flag_n = has_n ? ctl + 0 : nullptr;
+  const long long* flag_s = has_s ? ctl + 1 : nullptr;
+  unsigned* done = reinterpret_cast<unsigned*>(ctl + 2);
+  long long* pflag_n = has_n ? static_cast<long long*>(peers.north_control) + 1 : nullptr;
+  long long* pflag_s = has_s ? static_cast<long long*>(peers.south_control) + 0 : nullptr;
+  DeviceInfo info;
+  int dev = 0;
+  if (int rc = current_device_info(&info, &dev)) return rc;
+
+  HaloGeom g{};
+  g.pitch = pitch;
+  g.W = static_cast<int>(width);
+  g.h = static_cast<int>(rows);
+  g.north_rows = Sh;
+  g.south_rows = Nh;
+  g.north_off = has_n ? (Nh + peers.north_rows) * pitch : 0;
+  g.south_off = 0;
+  g.mode = d.border_mode;
+  const long long B = *epoch;
+  const long long inner = rows - 2LL * m;
+
+  // Resolve every kernel before the first launch (lazy loading; see the
+  // one-generation schedule).
+  {
+    KernelAttr ka;
+    if (int rc = kernel_attr(dev, halo_wait(), info, &ka)) return rc;
+    if (int rc = kernel_attr(dev, halo_put_kernel(d.dtype), info, &ka)) return rc;
+    CrossPlan cp;
+    const char* a0 = static_cast<const char*>(d_a) + Nh * row_bytes;
+    if (int rc = make_cross_plan(d, width, m, pitch, pitch, -Nh, m - 1 + Sh, wc, wr, TB, a0, a0, &cp)) return rc;
+    if (int rc = make_cross_plan(d, width, inner, pitch, pitch, -Nh, inner - 1 + Sh, wc, wr, TB, a0, a0, &cp)) {
+      return rc;
+    }
+  }
+  const int put_grid = static_cast<int>(std::max<long long>(
+      1, std::min<long long>((static_cast<long long>(Nh + Sh) * width + 255) / 256, 4LL * info.sms)));
+  auto put = [&](const void* src_rows, void* pn, void* ps, long long wait, long long signal) {
+    g.wait_value = wait;
+    g.signal_value = signal;
+    void* args[] = {const_cast<void**>(&src_rows), &pn, &ps, const_cast<long long**>(&flag_n),
+                    const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done, &g};
+    return launch_checked(halo_put_kernel(d.dtype), dim3(put_grid), dim3(256), args, 0, st);
+  };
+  // state-0 halos
+  if (int rc = put(static_cast<const char*>(d_a) + Nh * row_bytes, peers.north_a, peers.south_a, B, B + 1)) {
+    return rc;
+  }
+  void* src = d_a;
+  void* dst = d_b;
+  int launches = 0;
+  for (int done_gens = 0; done_gens < iterations; ++launches) {
+    const int tb = std::min(TB, iterations - done_gens);
+    const long long k = launches + 1;
+    {
+      long long value = B + k;
+      void* args[] = {const_cast<long long**>(&flag_n), const_cast<long long**>(&flag_s), &value};
+      if (int rc = launch_checked(halo_wait(), dim3(1), dim3(32), args, 0, st)) return rc;
+    }
+    const char* s0 = static_cast<const char*>(src) + Nh * row_bytes;
+    char* d0 = static_cast<char*>(dst) + Nh * row_bytes;
+    // top strip: reads the north halo (if any) and TB*S owned rows below it
+    if (int rc = run_cross(d, s0, d0, width, m, pitch, pitch, has_n ? Nh : 0, Sh, wc, wr, tb, st)) return rc;
+    // bottom strip
+    if (int rc = run_cross(d, s0 + (rows - m) * row_bytes, d0 + (rows - m) * row_bytes, width, m, pitch,
+                           pitch, Nh, has_s ? Sh : 0, wc, wr, tb, st)) {
+      return rc;
+    }
+    void* pn = has_n ? (k & 1 ? peers.north_b : peers.north_a) : nullptr;
+    void* ps = has_s ? (k & 1 ? peers.south_b : peers.south_a) : nullptr;
+    if (int rc = put(d0, pn, ps, B + k, B + k + 1)) return rc;
+    if (inner > 0) {
+      if (int rc = run_cross(d, s0 + m * row_bytes, d0 + m * row_bytes, width, inner, pitch, pitch, Nh, Sh,
+                             wc, wr, tb, st)) {
+        return rc;
+      }
+    }
+    done_gens += tb;
+    std::swap(src, dst);
+  }
+  *epoch = B + launches + 1;
+  if (result_in_b) *result_in_b = launches % 2;
+  return SK_OK;
+}
+
 }  // namespace
 }  // namespace sk
 
@@ -1422,8 +1539,12 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
   const sk_stencil_desc& d = *desc;
   if (!d_a || !d_b || !peers || !d_control || !epoch) return fail(SK_EINVAL, "null argument");
   if (iterations < 0) return fail(SK_EINVAL, "negative iterations");
+  if (uses_strips(d) && d.fused_iterations > 1) {
+    return iterate_peer_strips(d, d_a, d_b, width, rows, pitch, iterations, wc, wr, *peers,
+                               d_control, epoch, static_cast<cudaStream_t>(stream), result_in_b);
+  }
   if (d.fused_iterations > 1 || uses_bits(d) || uses_strips(d)) {
-    return fail(SK_ENOTSUP, "the peer-exchange schedule runs one generation per exchange");
+    return fail(SK_ENOTSUP, "the peer-exchange schedule fuses generations only on the register-strip path");
   }
   const int N = d.north, S = d.south;
   const int m = std::max(N, S);

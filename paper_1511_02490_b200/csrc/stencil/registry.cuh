@@ -50,5 +50,6 @@ KernelPtr halo_strips_f64(const sk_stencil_desc& d);
 KernelPtr halo_put_i32();
 KernelPtr halo_put_f32();
 KernelPtr halo_put_f64();
+KernelPtr halo_wait();
 
 }  // namespace sk

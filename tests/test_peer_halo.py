@@ -47,9 +47,11 @@ def grid(op, dtype, shape, seed):
 
 def run_ranks(st, x, world, iterations, wc=32, wr=8, calls=1):
     """P logical ranks on one GPU; `calls` consecutive iterate calls (the
-    epoch carries across them).  Returns the gathered grid."""
+    epoch carries across them).  Returns the gathered grid.  Temporally
+    blocked stencils (TB generations per exchange) get TB-deep halos."""
     H, W = x.shape
-    n, s = st.north, st.south
+    depth = max(1, st.fused_iterations)
+    n, s = depth * st.north, depth * st.south
     shards = [RowShard(H, W, p, world, n, s) for p in range(world)]
     bufs, streams = [], []
     for sh in shards:
@@ -120,10 +122,27 @@ def test_peer_exchange_config3_shape():
     assert got.tobytes() == want.tobytes()
 
 
-def test_peer_rejects_fused_paths():
-    st = Stencil(op="heat", dtype="float32", fused_iterations=8)
-    with pytest.raises(Exception):
-        run_ranks(st, grid("heat", "float32", (40, 40), 1), 2, 3)
+def test_peer_rejects_per_cell_fused_and_bitplane():
+    for st in (Stencil(op="heat", dtype="float32", fused_iterations=4, load_path="tma"),
+               Stencil(op="gol", dtype="int32", fused_iterations=8)):
+        with pytest.raises(Exception):
+            run_ranks(st, grid(st.op, st.dtype, (120, 40), 1), 2, 3)
+
+
+@pytest.mark.parametrize("op,dtype,border,pad", [("heat", "float32", "nearest", 0.0),
+                                                 ("five_point", "int32", "pad", 7.0),
+                                                 ("heat", "float64", "pad", 0.25)])
+@pytest.mark.parametrize("tb,world", [(4, 2), (8, 3), (5, 2)])
+def test_peer_exchange_temporal_blocking(op, dtype, border, pad, tb, world):
+    """Register-strip path, TB generations per exchange (TB-deep halos, the
+    strips / put / interior schedule of sk_stencil_iterate_peer), over three
+    consecutive calls whose generation counts are not multiples of TB."""
+    st = Stencil(op=op, dtype=dtype, border=border, pad_value=pad, load_path="strips",
+                 fused_iterations=tb)
+    x = grid(op, dtype, (world * 70, 333), seed=tb * 10 + world)
+    got = run_ranks(st, x, world, 29, wc=32, wr=8, calls=3)
+    want = O.iterate(O.desc_from_stencil(st), x, 29)
+    assert got.tobytes() == want.tobytes()
 
 
 def test_peer_exchange_two_processes_ipc():
