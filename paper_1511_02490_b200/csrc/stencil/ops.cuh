@@ -102,22 +102,40 @@ struct has_column<Op, std::void_t<decltype(Op::kColumn)>> : std::bool_constant<O
 struct Gol {
   static constexpr bool kColumn = true;
 
+  // alive(v) = v != 0 as 0/1: one unsigned min for int32 (any non-zero bit
+  // pattern, negatives included, maps to 1); floats drop the sign bit first
+  // so -0.0 stays dead and NaN stays alive, exactly like `v != 0`.
+  template <typename T>
+  __device__ __forceinline__ static unsigned alive(T v) {
+    if constexpr (std::is_same_v<T, int32_t>) {
+      return min(static_cast<unsigned>(v), 1u);
+    } else if constexpr (std::is_same_v<T, float>) {
+      return min(__float_as_uint(v) & 0x7fffffffu, 1u);
+    } else {
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+      return b != 0ull;
+    }
+  }
+
+  // Per row i: x = l + m + r (3-sum) and y = l + r (2-sum, the centre row's
+  // neighbours); the 8-neighbour count of cell k is x[k] + y[k+1] + x[k+2].
+  // B3/S23: alive next iff n8 == 3 or (alive and n8 == 2), i.e. (n8 | alive) == 3.
   template <typename T, int K>
   __device__ __forceinline__ void column(const T* centre, int pitch, const OpParams<T>&,
                                          T (&res)[K]) const {
-    int mid[K + 2];
-    int row[K + 2];
+    unsigned mid[K + 2], x[K + 2], y[K + 2];
 #pragma unroll
     for (int i = 0; i < K + 2; ++i) {
       const T* r = centre + (i - 1) * pitch;
-      const int l = r[-1] != T(0), m = r[0] != T(0), rr = r[1] != T(0);
+      const unsigned l = alive(r[-1]), m = alive(r[0]), rr = alive(r[1]);
       mid[i] = m;
-      row[i] = l + m + rr;
+      y[i] = l + rr;
+      x[i] = y[i] + m;
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int n = row[k] + row[k + 1] + row[k + 2] - mid[k + 1];
-      res[k] = (n == 3 || (mid[k + 1] && n == 2)) ? T(1) : T(0);
+      const unsigned n8 = x[k] + y[k + 1] + x[k + 2];
+      res[k] = ((n8 | mid[k + 1]) == 3u) ? T(1) : T(0);
     }
   }
 
