@@ -190,6 +190,19 @@ int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_o
                         int64_t width, int64_t height, int32_t iterations, int32_t wc,
                         int32_t wr);
 
+/* Streamed end-to-end jobs from HOST buffers (pinned for the copies to be
+ * asynchronous): sk_stencil_submit_host enqueues H2D of h_in, `iterations`
+ * passes and D2H into h_out on one of two internal slots (stream + device
+ * buffers) and returns a ticket without waiting, so the copies of one job
+ * run on the copy engines while the other job computes.  A submit waits only
+ * for the job two tickets back (its slot's buffers).  sk_stencil_wait_host
+ * blocks until job `ticket` has landed in its h_out.  Same results as
+ * sk_stencil_run_host, which is the one-job-at-a-time form. */
+int sk_stencil_submit_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,
+                           int64_t width, int64_t height, int32_t iterations, int32_t wc,
+                           int32_t wr, int64_t* ticket);
+int sk_stencil_wait_host(int64_t ticket);
+
 /* Device features (north-star subsystem 3): the DeviceDescriptor fields of
  * the reference (scenario.hpp:31-44) read from cudaDeviceProp instead of the
  * OpenCL device API. */

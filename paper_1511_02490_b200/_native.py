@@ -120,6 +120,9 @@ _PROTOTYPES = {
     "sk_stencil_time": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32,
                                ctypes.POINTER(ctypes.c_double)]),
     "sk_stencil_run_host": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i32, _i32, _i32]),
+    "sk_stencil_submit_host": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i32, _i32, _i32,
+                                      ctypes.POINTER(_i64)]),
+    "sk_stencil_wait_host": (_i32, [_i64]),
     "sk_device_features": (_i32, [_i32, ctypes.POINTER(sk_device_props)]),
     "sk_fill_host": (_i32, [_i32, _i32, ctypes.c_uint64, _vp, _i64]),
     "sk_buffers_equal": (_i32, [_vp, _vp, _i64, ctypes.POINTER(_i32)]),

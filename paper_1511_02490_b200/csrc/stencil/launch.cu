@@ -957,6 +957,18 @@ struct Scratch {
   std::vector<cudaEvent_t> events;
   void* bits[2] = {nullptr, nullptr};  // packed bit grids of the chained gol path
   size_t bits_bytes = 0;
+  // streamed host jobs (sk_stencil_submit_host): two slots, each with its own
+  // stream, device ping-pong buffers and completion event
+  struct Slot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    void* a = nullptr;
+    void* b = nullptr;
+    size_t bytes = 0;
+    long long ticket = -1;  // job in flight (or last completed)
+    int status = SK_OK;
+  } slots[2];
+  long long next_ticket = 0;
 };
 // Per (device, calling thread): the timing stream, event pool, flush buffer
 // and e2e staging buffers are never shared between threads (reentrant ABI).
@@ -1386,6 +1398,70 @@ int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_o
   cudaMemcpyAsync(h_out, in_b ? s->dev_b : s->dev_a, bytes, cudaMemcpyDeviceToHost, s->stream);
   cudaError_t e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return fail(SK_ECUDA, "run_host failed: %s", cudaGetErrorString(e));
+  return SK_OK;
+}
+
+int sk_stencil_submit_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,
+                           int64_t width, int64_t height, int32_t iterations, int32_t wc,
+                           int32_t wr, int64_t* ticket) {
+  g_last_error.clear();
+  if (int rc = validate_desc(desc)) return rc;
+  if (!h_in || !h_out || !ticket) return fail(SK_EINVAL, "null argument");
+  if (width < 1 || height < 1) return fail(SK_EINVAL, "bad dims");
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  const long long t = s->next_ticket;
+  Scratch::Slot& sl = s->slots[t & 1];
+  if (!sl.stream) {
+    if (cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
+      return fail(SK_ECUDA, "slot stream/event creation failed");
+    }
+  }
+  // the slot's previous job (ticket t - 2) must be finished before its
+  // buffers are reused: a host wait only when the caller runs ahead
+  if (sl.ticket >= 0) {
+    cudaError_t e = cudaEventSynchronize(sl.done);
+    if (e != cudaSuccess) return fail(SK_ECUDA, "previous job failed: %s", cudaGetErrorString(e));
+  }
+  const size_t bytes = static_cast<size_t>(width) * height * dtype_size(desc->dtype);
+  if (sl.bytes < bytes) {
+    cudaFree(sl.a);
+    cudaFree(sl.b);
+    sl.a = sl.b = nullptr;
+    sl.bytes = 0;
+    if (cudaMalloc(&sl.a, bytes) != cudaSuccess || cudaMalloc(&sl.b, bytes) != cudaSuccess) {
+      return fail(SK_ECUDA, "device buffer allocation failed (%zu B)", bytes);
+    }
+    sl.bytes = bytes;
+  }
+  cudaMemcpyAsync(sl.a, h_in, bytes, cudaMemcpyHostToDevice, sl.stream);
+  int32_t in_b = 0;
+  if (int rc = sk_stencil_iterate(desc, sl.a, sl.b, width, height, width, iterations, wc, wr,
+                                  sl.stream, &in_b)) {
+    return rc;
+  }
+  cudaMemcpyAsync(h_out, in_b ? sl.b : sl.a, bytes, cudaMemcpyDeviceToHost, sl.stream);
+  cudaError_t e = cudaEventRecord(sl.done, sl.stream);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "submit failed: %s", cudaGetErrorString(e));
+  sl.ticket = t;
+  s->next_ticket = t + 1;
+  *ticket = t;
+  return SK_OK;
+}
+
+int sk_stencil_wait_host(int64_t ticket) {
+  g_last_error.clear();
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  if (ticket < 0 || ticket >= s->next_ticket) return fail(SK_EINVAL, "unknown ticket %lld", (long long)ticket);
+  Scratch::Slot& sl = s->slots[ticket & 1];
+  if (sl.ticket != ticket) {
+    // the slot has moved on: a later submit already waited for this job
+    return ticket < sl.ticket ? SK_OK : fail(SK_EINVAL, "ticket %lld not in flight", (long long)ticket);
+  }
+  cudaError_t e = cudaEventSynchronize(sl.done);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "job %lld failed: %s", (long long)ticket, cudaGetErrorString(e));
   return SK_OK;
 }
 

@@ -193,6 +193,23 @@ class Stencil:
             self._raise(rc, "sk_stencil_run_host", wc, wr)
 
 
+    def submit_host(self, h_in, h_out, iterations: int, wc: int, wr: int) -> int:
+        """Streamed end-to-end job (pinned host buffers): returns a ticket
+        immediately; at most two jobs are in flight per thread."""
+        t = ctypes.c_int64(-1)
+        height, width = h_in.shape
+        rc = N.lib().sk_stencil_submit_host(ctypes.byref(self._desc), _host_ptr(h_in),
+                                            _host_ptr(h_out), width, height, iterations, wc, wr,
+                                            ctypes.byref(t))
+        if rc:
+            self._raise(rc, "sk_stencil_submit_host", wc, wr)
+        return t.value
+
+    @staticmethod
+    def wait_host(ticket: int) -> None:
+        N.check(N.lib().sk_stencil_wait_host(ticket), "sk_stencil_wait_host")
+
+
 def _host_ptr(a) -> int:
     if hasattr(a, "data_ptr"):
         return a.data_ptr()

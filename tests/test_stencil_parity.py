@@ -339,3 +339,32 @@ def test_in_process_autotuner_prediction_is_legal():
     assert r["wc"] * r["wr"] <= 1024 and r["probes"] >= 1
     x = rand_grid("int32", (2000, 3000), 4, "gol")
     assert_same(gpu_pass(st, x, r["wc"], r["wr"]), O.stencil(O.desc_from_stencil(st), x), "predicted")
+
+
+@pytest.mark.gpu
+def test_streamed_host_jobs_match_run_host():
+    """sk_stencil_submit_host / sk_stencil_wait_host (two slots in flight)
+    give the same bytes as sk_stencil_run_host, for interleaved jobs of
+    different inputs, sizes and iteration counts."""
+    import torch
+
+    st = Stencil(op="heat", dtype="float32", border="nearest")
+    rng = np.random.default_rng(4)
+    jobs = [(rng.random((300, 257)).astype(np.float32), 7), (rng.random((64, 900)).astype(np.float32), 4),
+            (rng.random((300, 257)).astype(np.float32), 1), (rng.random((5, 5)).astype(np.float32), 3)]
+    ins = [torch.from_numpy(x).pin_memory() for x, _ in jobs]
+    outs = [torch.empty_like(t).pin_memory() for t in ins]
+    tickets = []
+    for (x, it), hi, ho in zip(jobs, ins, outs):
+        if len(tickets) >= 2:
+            st.wait_host(tickets[-2])
+        tickets.append(st.submit_host(hi, ho, it, 32, 8))
+    for t in tickets:
+        st.wait_host(t)
+    for (x, it), ho in zip(jobs, outs):
+        want = np.empty_like(x)
+        st.run_host(x, want, it, 32, 8)
+        assert ho.numpy().tobytes() == want.tobytes()
+        assert want.tobytes() == O.iterate(O.desc_from_stencil(st), x, it).tobytes()
+    with pytest.raises(Exception):
+        st.wait_host(10 ** 9)
