@@ -351,20 +351,20 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
     import torch
 
     if world == 1:
-        # Streamed jobs (sk_stencil_submit_host): two in flight, so one job's
-        # H2D / D2H run on the copy engines while the other computes.  Every
-        # step still copies its input in and its result out.
-        h_in = [torch.from_numpy(host).pin_memory() for _ in range(2)]
-        h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(2)]
-        for j in range(2):  # warm-up (allocates the slots' device buffers)
+        # Streamed jobs (sk_stencil_submit_host): three in flight, so job
+        # j+1's H2D and job j-1's D2H run on the copy engines while job j
+        # computes.  Every step still copies its input in and its result out.
+        h_in = [torch.from_numpy(host).pin_memory() for _ in range(3)]
+        h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(3)]
+        for j in range(3):  # warm-up (allocates the slots' device buffers)
             st.wait_host(st.submit_host(h_in[j], h_out[j], iters, wc, wr))
-        k = max(4, min(args.steps, 8))
+        k = max(6, min(args.steps, 12))
         tickets = []
         t0 = time.perf_counter()
         for j in range(k):
-            if len(tickets) >= 2:
+            if len(tickets) >= 3:
                 st.wait_host(tickets.pop(0))
-            tickets.append(st.submit_host(h_in[j % 2], h_out[j % 2], iters, wc, wr))
+            tickets.append(st.submit_host(h_in[j % 3], h_out[j % 3], iters, wc, wr))
         for t in tickets:
             st.wait_host(t)
         dt = time.perf_counter() - t0
@@ -375,7 +375,7 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
         sync_value = host.size * iters / (time.perf_counter() - t1) / 1e9
         return {"value": round(host.size * iters * k / dt / 1e9, 3), "unit": "Gcells/s",
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                "steps": k, "api": "sk_stencil_submit_host / sk_stencil_wait_host (2 jobs in flight)",
+                "steps": k, "api": "sk_stencil_submit_host / sk_stencil_wait_host (3 jobs in flight)",
                 "synchronous_run_host_value": round(sync_value, 3)}
     import torch.distributed as dist
 

@@ -192,10 +192,10 @@ int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_o
 
 /* Streamed end-to-end jobs from HOST buffers (pinned for the copies to be
  * asynchronous): sk_stencil_submit_host enqueues H2D of h_in, `iterations`
- * passes and D2H into h_out on one of two internal slots (stream + device
- * buffers) and returns a ticket without waiting, so the copies of one job
- * run on the copy engines while the other job computes.  A submit waits only
- * for the job two tickets back (its slot's buffers).  sk_stencil_wait_host
+ * passes and D2H into h_out on one of three internal slots (stream + device
+ * buffers) and returns a ticket without waiting, so job j+1's H2D and job
+ * j-1's D2H run on the copy engines while job j computes.  A submit waits
+ * only for the job three tickets back (its slot's buffers).  sk_stencil_wait_host
  * blocks until job `ticket` has landed in its h_out.  Same results as
  * sk_stencil_run_host, which is the one-job-at-a-time form. */
 int sk_stencil_submit_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,

@@ -6,6 +6,8 @@
 //   wgtb::Stencil<float> blur(SK_OP_GAUSSIAN, {5, 5, 5, 5}, wgtb::Border::nearest());
 //   blur(d_in, d_out, W, H, /*wc=*/32, /*wr=*/8);               // one pass
 //   blur.iterate(d_a, d_b, W, H, 100, 32, 8);                   // ping-pong
+//   wgtb::Stencil<float> heat(SK_OP_HEAT, {}, wgtb::Border::nearest());
+//   heat.load_path(SK_LOAD_STRIPS).fused_iterations(8).iterate(d_a, d_b, W, H, 100, 32, 12);
 //
 // Errors follow the reference's taxonomy (errors.hpp): IllegalWorkgroupSize
 // for wc*wr above the maximum, RefusedParameter(w_c, w_r) for a refused
@@ -80,6 +82,12 @@ class Stencil {
     desc_.load_path = p;
     return *this;
   }
+  // Temporal blocking: TB generations per launch (per-cell fused 2/4,
+  // bit-plane GoL 1..128, register-strip cross ops 1..32; sk_stencil.h).
+  Stencil& fused_iterations(int tb) {
+    desc_.fused_iterations = tb;
+    return *this;
+  }
 
   // One pass over a W x H device grid (row pitch in elements; 0 = W).
   void operator()(const T* d_in, T* d_out, int64_t W, int64_t H, int wc, int wr,
@@ -104,6 +112,19 @@ class Stencil {
   void run_host(const T* h_in, T* h_out, int64_t W, int64_t H, int iterations, int wc, int wr) const {
     throw_status(sk_stencil_run_host(&desc_, h_in, h_out, W, H, iterations, wc, wr), wc, wr,
                  "Stencil::run_host");
+  }
+
+  // Streamed host jobs (pinned buffers): submit returns a ticket at once,
+  // three jobs in flight per thread; wait blocks until h_out holds the result.
+  int64_t submit_host(const T* h_in, T* h_out, int64_t W, int64_t H, int iterations, int wc,
+                      int wr) const {
+    int64_t ticket = -1;
+    throw_status(sk_stencil_submit_host(&desc_, h_in, h_out, W, H, iterations, wc, wr, &ticket), wc,
+                 wr, "Stencil::submit_host");
+    return ticket;
+  }
+  static void wait_host(int64_t ticket) {
+    throw_status(sk_stencil_wait_host(ticket), 0, 0, "Stencil::wait_host");
   }
 
   // Legality without launching: SK_OK, SK_OVERSIZED or SK_REFUSED.

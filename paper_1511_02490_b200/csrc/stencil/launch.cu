@@ -957,8 +957,9 @@ struct Scratch {
   std::vector<cudaEvent_t> events;
   void* bits[2] = {nullptr, nullptr};  // packed bit grids of the chained gol path
   size_t bits_bytes = 0;
-  // streamed host jobs (sk_stencil_submit_host): two slots, each with its own
-  // stream, device ping-pong buffers and completion event
+  // streamed host jobs (sk_stencil_submit_host): three slots, each with its
+  // own stream, device ping-pong buffers and completion event, so job j+1's
+  // H2D, job j's passes and job j-1's D2H can all be in flight at once
   struct Slot {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
@@ -967,7 +968,7 @@ struct Scratch {
     size_t bytes = 0;
     long long ticket = -1;  // job in flight (or last completed)
     int status = SK_OK;
-  } slots[2];
+  } slots[3];
   long long next_ticket = 0;
 };
 // Per (device, calling thread): the timing stream, event pool, flush buffer
@@ -1411,14 +1412,14 @@ int sk_stencil_submit_host(const sk_stencil_desc* desc, const void* h_in, void* 
   Scratch* s = nullptr;
   if (int rc = scratch(&s)) return rc;
   const long long t = s->next_ticket;
-  Scratch::Slot& sl = s->slots[t & 1];
+  Scratch::Slot& sl = s->slots[t % 3];
   if (!sl.stream) {
     if (cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
       return fail(SK_ECUDA, "slot stream/event creation failed");
     }
   }
-  // the slot's previous job (ticket t - 2) must be finished before its
+  // the slot's previous job (ticket t - 3) must be finished before its
   // buffers are reused: a host wait only when the caller runs ahead
   if (sl.ticket >= 0) {
     cudaError_t e = cudaEventSynchronize(sl.done);
@@ -1455,7 +1456,7 @@ int sk_stencil_wait_host(int64_t ticket) {
   Scratch* s = nullptr;
   if (int rc = scratch(&s)) return rc;
   if (ticket < 0 || ticket >= s->next_ticket) return fail(SK_EINVAL, "unknown ticket %lld", (long long)ticket);
-  Scratch::Slot& sl = s->slots[ticket & 1];
+  Scratch::Slot& sl = s->slots[ticket % 3];
   if (sl.ticket != ticket) {
     // the slot has moved on: a later submit already waited for this job
     return ticket < sl.ticket ? SK_OK : fail(SK_EINVAL, "ticket %lld not in flight", (long long)ticket);

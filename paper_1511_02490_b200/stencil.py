@@ -195,7 +195,7 @@ class Stencil:
 
     def submit_host(self, h_in, h_out, iterations: int, wc: int, wr: int) -> int:
         """Streamed end-to-end job (pinned host buffers): returns a ticket
-        immediately; at most two jobs are in flight per thread."""
+        immediately; at most three jobs are in flight per thread."""
         t = ctypes.c_int64(-1)
         height, width = h_in.shape
         rc = N.lib().sk_stencil_submit_host(ctypes.byref(self._desc), _host_ptr(h_in),

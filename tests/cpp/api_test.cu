@@ -98,6 +98,32 @@ int main() {
     CHECK(r[19 * n + 31] == 1 && r[20 * n + 31] == 1 && r[21 * n + 31] == 1 && r[20 * n + 30] == 0,
           "gol run_host one step wrong");
     CHECK(gol.probe(n, n, 64, 32) == SK_OVERSIZED, "probe should report oversized");
+    // temporally blocked paths through the same API: bit-plane GoL (TB 8) and
+    // streamed host jobs must reproduce the one-pass results
+    wgtb::Stencil<int32_t> bits(SK_OP_GOL, {1, 1, 1, 1}, wgtb::Border::padding(0));
+    bits.load_path(SK_LOAD_BITPLANE).fused_iterations(8);
+    cudaMemcpy(a, b.data(), n * n * 4, cudaMemcpyHostToDevice);
+    res = bits.iterate(a, bb, n, n, 10, 32, 8);
+    cudaMemcpy(r.data(), res, n * n * 4, cudaMemcpyDeviceToHost);
+    CHECK(r == b, "bit-plane gol blinker not periodic");
+    std::vector<int32_t> r1(n * n), r2(n * n);
+    const int64_t t1 = gol.submit_host(b.data(), r1.data(), n, n, 1, 8, 8);
+    const int64_t t2 = gol.submit_host(b.data(), r2.data(), n, n, 2, 8, 8);
+    wgtb::Stencil<int32_t>::wait_host(t1);
+    wgtb::Stencil<int32_t>::wait_host(t2);
+    CHECK(r1[19 * n + 31] == 1 && r1[20 * n + 30] == 0 && r2 == b, "streamed host jobs wrong");
+  }
+  // register-strip heat (TB 6) equals six one-pass generations
+  {
+    const int W = 300, H = 97;
+    std::vector<float> h(W * H), o1(W * H), o2(W * H);
+    for (int i = 0; i < W * H; ++i) h[i] = static_cast<float>((i * 2654435761u) % 1000) / 1000.0f;
+    wgtb::Stencil<float> one(SK_OP_HEAT, {}, wgtb::Border::nearest());
+    wgtb::Stencil<float> tb(SK_OP_HEAT, {}, wgtb::Border::nearest());
+    tb.load_path(SK_LOAD_STRIPS).fused_iterations(6);
+    one.run_host(h.data(), o1.data(), W, H, 13, 32, 8);
+    tb.run_host(h.data(), o2.data(), W, H, 13, 32, 12);
+    CHECK(o1 == o2, "strip heat differs from one-pass");
   }
   std::printf(fails ? "FAILED %d\n" : "OK\n", fails);
   return fails ? 1 : 0;

@@ -343,7 +343,7 @@ def test_in_process_autotuner_prediction_is_legal():
 
 @pytest.mark.gpu
 def test_streamed_host_jobs_match_run_host():
-    """sk_stencil_submit_host / sk_stencil_wait_host (two slots in flight)
+    """sk_stencil_submit_host / sk_stencil_wait_host (three slots in flight)
     give the same bytes as sk_stencil_run_host, for interleaved jobs of
     different inputs, sizes and iteration counts."""
     import torch
@@ -351,13 +351,14 @@ def test_streamed_host_jobs_match_run_host():
     st = Stencil(op="heat", dtype="float32", border="nearest")
     rng = np.random.default_rng(4)
     jobs = [(rng.random((300, 257)).astype(np.float32), 7), (rng.random((64, 900)).astype(np.float32), 4),
-            (rng.random((300, 257)).astype(np.float32), 1), (rng.random((5, 5)).astype(np.float32), 3)]
+            (rng.random((300, 257)).astype(np.float32), 1), (rng.random((5, 5)).astype(np.float32), 3),
+            (rng.random((129, 40)).astype(np.float32), 2)]
     ins = [torch.from_numpy(x).pin_memory() for x, _ in jobs]
     outs = [torch.empty_like(t).pin_memory() for t in ins]
     tickets = []
     for (x, it), hi, ho in zip(jobs, ins, outs):
-        if len(tickets) >= 2:
-            st.wait_host(tickets[-2])
+        if len(tickets) >= 3:
+            st.wait_host(tickets[-3])
         tickets.append(st.submit_host(hi, ho, it, 32, 8))
     for t in tickets:
         st.wait_host(t)
