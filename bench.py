@@ -239,10 +239,22 @@ def run_ours(args):
     step_fn = cuda_step(st, wc, wr)
     stream = torch.cuda.current_stream()
     links = None
+    transport = args.transport if world > 1 else None
     if world > 1 and args.transport == "peer":
         from paper_1511_02490_b200.distributed import connect_peers, iterate_sharded_peer, new_control
 
-        links = connect_peers(a, b, new_control(), shard)
+        try:
+            links = connect_peers(a, b, new_control(), shard)
+            ok = 1
+        except Exception as exc:  # e.g. allocations IPC cannot export: use NCCL, say so
+            ok, why = 0, str(exc).splitlines()[0][:160]
+        flag = torch.tensor([ok], device="cuda" if args.backend == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag[0]) == 0:
+            if links is not None:
+                links.close()
+            links = None
+            transport = "nccl (peer mapping unavailable" + (f": {why})" if not ok else ")")
 
     def one_step():
         if links is not None:
@@ -322,7 +334,8 @@ def run_ours(args):
                 "l2": f"inputs larger than L2 ({shard.rows * W * es / 1e6:.0f} MB per buffer)",
                 "parallelism": f"row-shard x{world}" + (
                     (" + peer-memory halo exchange fused into the strip kernel"
-                     if args.transport == "peer" else " + NCCL halo exchange") if world > 1 else ""),
+                     if links is not None else " + NCCL halo exchange") if world > 1 else ""),
+                "transport": "peer" if links is not None else transport,
             },
             "hbm_frac": round(achieved / peak, 4),
             "predicted_over_oracle": sweep_info.get("predicted_over_oracle"),
