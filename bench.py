@@ -304,6 +304,8 @@ def run_ours(args):
     temporal = None
     if rank == 0 and world == 1 and not args.no_temporal:
         temporal = temporal_leg(args, host, tdt, wc, wr, iters, peak)
+    elif world > 1 and args.config == "heat" and links is not None and not args.no_temporal:
+        temporal = temporal_leg_sharded(args, host, shard, wc, wr, iters, world, rank)
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -503,6 +505,61 @@ def temporal_leg(args, host, tdt, wc1, wr1, iters, peak):
         except Exception:
             pass
     return out
+
+
+def temporal_leg_sharded(args, host, shard, wc1, wr1, iters, world, rank,
+                         tb=8, k=8, wc=32, wr=12):
+    """Config 3 across ranks on the register-strip path: TB generations per
+    exchange over TB-deep halos (sk_stencil_iterate_peer's temporally blocked
+    schedule).  Checked bit-exact against the one-generation peer schedule on
+    the same input, then timed like the headline (CUDA events, max over
+    ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1511_02490_b200 import Stencil
+    from paper_1511_02490_b200.distributed import (RowShard, connect_peers, iterate_sharded_peer,
+                                                   new_control)
+
+    op, dtype, _, W, _, border, pad, (n, s, e, w) = CONFIGS[args.config]
+    x = torch.from_numpy(host).cuda()
+
+    def buffers(depth_n, depth_s):
+        sh = RowShard(shard.height, W, rank, world, depth_n, depth_s)
+        a = torch.zeros((sh.buffer_rows, W), dtype=x.dtype, device="cuda")
+        a[depth_n:depth_n + sh.rows] = x
+        b = torch.zeros_like(a)
+        return sh, a, b, connect_peers(a, b, new_control(), sh)
+
+    one = Stencil(op=op, dtype=dtype, border=border, pad_value=pad)
+    sh1, a1, b1, l1 = buffers(n, s)
+    want = sh1.owned(iterate_sharded_peer(a1, b1, sh1, iters, one, wc1, wr1, l1)).clone()
+    st = Stencil(op=op, dtype=dtype, border=border, pad_value=pad, load_path="strips",
+                 fused_iterations=tb, cells_per_thread=k)
+    sht, at, bt, lt = buffers(tb * n, tb * s)
+    got = sht.owned(iterate_sharded_peer(at, bt, sht, iters, st, wc, wr, lt))
+    ok = torch.tensor([int(torch.equal(got, want))], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    for _ in range(args.warmup):
+        iterate_sharded_peer(at, bt, sht, iters, st, wc, wr, lt)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        iterate_sharded_peer(at, bt, sht, iters, st, wc, wr, lt)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    l1.close()
+    lt.close()
+    return {"value": round(float(shard.height) * W * iters / (ms / 1e3) / 1e9, 1), "unit": "Gcells/s",
+            "ms_per_step": round(ms, 4), "path": "strips + peer exchange every TB generations",
+            "generations_per_launch": tb, "cells_per_thread": k, "block": f"{wc}x{wr}",
+            "bit_exact_vs_one_pass": bool(int(ok[0])),
+            "note": "TB-deep halos; one wait / strip / put / interior round per TB generations"}
 
 
 # --------------------------------------------------------------- CPU side

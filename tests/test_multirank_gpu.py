@@ -38,3 +38,16 @@ def test_bench_two_ranks_json_line(transport):
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_grid"] == "8192x16384"
     assert d["e2e"]["value"] > 0
     assert ("peer-memory" in d["config"]["parallelism"]) == (transport == "peer")
+
+
+def test_bench_two_ranks_heat_temporal_leg():
+    """Config 3 at N=2 (ranks sharing the GPU): the headline peer schedule and
+    the temporally blocked peer schedule (TB-deep halos) agree bit for bit."""
+    proc = torchrun(2, "bench.py", "--gpus", "2", "--config", "heat", "--steps", "1", "--warmup", "3",
+                    "--wc", "104", "--wr", "6", "--no-cpu", "--no-e2e", "--backend", "gloo", timeout=900)
+    lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
+    assert proc.returncode == 0 and len(lines) == 1, proc.stdout + proc.stderr[-3000:]
+    d = json.loads(lines[0])
+    assert d["config"]["transport"] == "peer"
+    t = d["temporal_blocking"]
+    assert t and t["bit_exact_vs_one_pass"] and t["value"] > 0
