@@ -995,6 +995,33 @@ int scratch(Scratch** out) {
   return SK_OK;
 }
 
+// Fork/join lane of a caller's stream for the peer schedule: the interior
+// launch of a generation runs on `side` while the caller's stream runs the
+// boundary strips (which may wait on a neighbour's flag).  Keyed by (device,
+// caller stream): ranks sharing a process each bring their own stream, and
+// one shared side stream would serialise their interiors into a cycle.
+struct SideLane {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::map<std::pair<int, cudaStream_t>, SideLane> g_side;
+
+int side_lane(cudaStream_t st, SideLane** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SK_ECUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(g_mu);
+  SideLane& l = g_side[{dev, st}];
+  if (!l.side) {
+    if (cudaStreamCreateWithFlags(&l.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming) != cudaSuccess) {
+      return fail(SK_ECUDA, "side stream/event creation failed");
+    }
+  }
+  *out = &l;
+  return SK_OK;
+}
+
 // Packed ping-pong grids of the bit-plane path (per device and thread, kept
 // and grown as needed; freed with the process).
 int scratch_bits(long long words, void** p0, void** p1) {
@@ -1696,6 +1723,14 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
   }
   const int strip_grid = static_cast<int>(
       std::max<long long>(1, std::min<long long>((static_cast<long long>(m) * width + 255) / 256, 2LL * info.sms)));
+  // Per generation the strips (caller's stream) and the interior (side
+  // stream) run concurrently; a fork/join event pair orders generation g+1
+  // after both halves of generation g (each half reads the other's rows).
+  const long long inner = rows - 2LL * m;
+  SideLane* lane = nullptr;
+  if (inner > 0 && m > 0) {
+    if (int rc = side_lane(st, &lane)) return rc;
+  }
   void* src = d_a;
   void* dst = d_b;
   for (int gen = 1; gen <= iterations; ++gen) {
@@ -1705,6 +1740,12 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
     void* ps = has_s ? (gen & 1 ? peers->south_b : peers->south_a) : nullptr;
     const void* s0 = static_cast<const char*>(src) + N * row_bytes;
     void* d0 = static_cast<char*>(dst) + N * row_bytes;
+    cudaStream_t ist = st;
+    if (lane) {
+      cudaEventRecord(lane->fork, st);
+      cudaStreamWaitEvent(lane->side, lane->fork, 0);
+      ist = lane->side;
+    }
     if (m > 0) {
       int rc;
       switch (d.dtype) {
@@ -1720,12 +1761,15 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
       if (rc) return rc;
     }
     // interior rows [m, rows - m) read only owned rows (m >= N, S)
-    const long long inner = rows - 2LL * m;
     if (inner > 0) {
       if (int rc = launch(d, static_cast<const char*>(s0) + m * row_bytes, static_cast<char*>(d0) + m * row_bytes,
-                          width, inner, pitch, pitch, N, S, wc, wr, st)) {
+                          width, inner, pitch, pitch, N, S, wc, wr, ist)) {
         return rc;
       }
+    }
+    if (lane) {
+      cudaEventRecord(lane->join, lane->side);
+      cudaStreamWaitEvent(st, lane->join, 0);
     }
     std::swap(src, dst);
   }
