@@ -25,6 +25,27 @@
 
 namespace sk {
 
+// Peer-memory halo exchange fused into the one-pass kernel (PEER
+// instantiations only; zero otherwise).  The first and last tile-rows are
+// processed first: their TMA loads wait for the neighbours' arrival flags,
+// their first `north_rows` / last `south_rows` output rows are also stored
+// into the neighbours' halo rows, and the last of them publishes
+// `signal_value`.
+struct PeerTile {
+  const long long* flag_n;   // this rank's arrival flags (null: no neighbour)
+  const long long* flag_s;
+  long long wait_value;
+  void* peer_n;              // neighbours' dst buffers (base = their halo row 0)
+  void* peer_s;
+  long long north_off, south_off;  // elements
+  int north_rows, south_rows;
+  long long* pflag_n;        // neighbours' flags this rank publishes to
+  long long* pflag_s;
+  unsigned* done;            // boundary-tile ticket counter
+  long long signal_value;
+  int boundary_tiles;
+};
+
 // Launch geometry, computed on the host (launch.cu) for one (desc, W, H, wc, wr).
 struct Geom {
   int W, H;                 // computed region (columns, rows)
@@ -54,6 +75,7 @@ struct Geom {
   int bN, bS, bE, bW;
   int sp;                   // row pitch of the two scratch generation buffers
   int scratch_elems;        // elements per scratch buffer (incl. K slack rows)
+  PeerTile peer;            // fused peer exchange (PEER kernels only)
 };
 
 // ------------------------------------------------------------------ PTX glue
@@ -186,6 +208,79 @@ __device__ __forceinline__ void compute_tile(const T* tile, const Geom& g,
   }
 }
 
+// Fused peer exchange: boundary tile-rows first (row order 0, last, 1, 2, ...).
+__device__ __forceinline__ int peer_tile_row(const Geom& g, int ty) {
+  if (g.tiles_y < 2) return ty;
+  return ty == 0 ? 0 : (ty == 1 ? g.tiles_y - 1 : ty - 1);
+}
+
+__device__ __forceinline__ bool peer_boundary_row(const Geom& g, int tyr) {
+  return tyr == 0 || tyr == g.tiles_y - 1;
+}
+
+__device__ __forceinline__ long long ld_acquire_sys_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Producer side: a boundary tile's box includes halo rows, so its TMA load
+// waits for the neighbour's flag; the acquire is then ordered before the
+// async-proxy (TMA) reads of those rows.
+__device__ __forceinline__ void peer_wait_rows(const Geom& g, int tyr) {
+  bool waited = false;
+  if (tyr == 0 && g.peer.flag_n) {
+    while (ld_acquire_sys_s64(g.peer.flag_n) < g.peer.wait_value) __nanosleep(32);
+    waited = true;
+  }
+  if (tyr == g.tiles_y - 1 && g.peer.flag_s) {
+    while (ld_acquire_sys_s64(g.peer.flag_s) < g.peer.wait_value) __nanosleep(32);
+    waited = true;
+  }
+  if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Consumer side, after a boundary tile's stores: the threads that stored
+// into a neighbour's halo make those stores visible system-wide, then the
+// last boundary tile of the grid publishes the generation to the neighbours.
+// Nothing to publish (no neighbours): no fence, no barrier.
+__device__ __forceinline__ void peer_tile_done(const Geom& g, int tid, bool stored_peer) {
+  if (!g.peer.pflag_n && !g.peer.pflag_s) return;
+  if (stored_peer) __threadfence_system();
+  __syncthreads();
+  if (tid == 0 && atomicAdd(g.peer.done, 1u) == static_cast<unsigned>(g.peer.boundary_tiles) - 1u) {
+    __threadfence_system();
+    if (g.peer.pflag_n) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(g.peer.pflag_n), "l"(g.peer.signal_value) : "memory");
+    if (g.peer.pflag_s) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(g.peer.pflag_s), "l"(g.peer.signal_value) : "memory");
+    atomicExch(g.peer.done, 0u);
+  }
+}
+
+// Returns whether this thread stored into a neighbour's halo.
+template <typename T, int K>
+__device__ __forceinline__ bool store_peer_rows(const Geom& g, int r0, int c0, const T (&res)[K]) {
+  const int c = c0 + threadIdx.x;
+  const int r = r0 + threadIdx.y * K;
+  if (c >= g.W) return false;
+  T* pn = static_cast<T*>(g.peer.peer_n);
+  T* ps = static_cast<T*>(g.peer.peer_s);
+  bool stored = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int rr = r + j;
+    if (rr >= g.H) break;
+    if (pn && rr < g.peer.north_rows) {
+      pn[g.peer.north_off + static_cast<long long>(rr) * g.pitch_out + c] = res[j];
+      stored = true;
+    }
+    if (ps && rr >= g.H - g.peer.south_rows) {
+      ps[g.peer.south_off + static_cast<long long>(rr - (g.H - g.peer.south_rows)) * g.pitch_out + c] = res[j];
+      stored = true;
+    }
+  }
+  return stored;
+}
+
 template <typename T, int K>
 __device__ __forceinline__ void store_tile(T* __restrict__ out, const Geom& g, int r0, int c0,
                                            bool edge, const T (&res)[K]) {
@@ -204,11 +299,15 @@ __device__ __forceinline__ void store_tile(T* __restrict__ out, const Geom& g, i
 }
 
 // --------------------------------------------------------------------- K1a
-template <typename T>
+template <typename T, bool PEER = false>
 __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage, uint64_t* bar,
                                                const Geom& g, int t) {
   int ty = t / g.tiles_x;
   int tx = t - ty * g.tiles_x;
+  if constexpr (PEER) {
+    ty = peer_tile_row(g, ty);
+    peer_wait_rows(g, ty);
+  }
   int x = tx * g.wc - g.Wb;
   x -= x & (g.vec - 1);                      // 16-B aligned innermost start
   int y = ty * g.tile_rows - g.N + g.above;  // tensor rows start `above` rows before row 0
@@ -218,7 +317,7 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage,
   }
 }
 
-template <class Op, typename T, int K, int MAXT>
+template <class Op, typename T, int K, int MAXT, bool PEER = false>
 __global__ void __launch_bounds__(MAXT)
     k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
                   const T pad, const __grid_constant__ OpParams<T> p) {
@@ -251,7 +350,7 @@ __global__ void __launch_bounds__(MAXT)
     for (int s = 0; s < g.stages; ++s) {
       int t = blockIdx.x + s * gridDim.x;
       if (t < ntiles) {
-        tma_issue_tile<T>(&map, reinterpret_cast<T*>(smem + s * g.stage_bytes), &full[s], g, t);
+        tma_issue_tile<T, PEER>(&map, reinterpret_cast<T*>(smem + s * g.stage_bytes), &full[s], g, t);
       }
     }
   }
@@ -274,7 +373,7 @@ __global__ void __launch_bounds__(MAXT)
       int tn = t + (g.stages - lag) * gridDim.x;
       if (tn < ntiles) {
         mbar_wait_parity(&empty[ps], pphase);
-        tma_issue_tile<T>(&map, reinterpret_cast<T*>(smem + ps * g.stage_bytes), &full[ps], g,
+        tma_issue_tile<T, PEER>(&map, reinterpret_cast<T*>(smem + ps * g.stage_bytes), &full[ps], g,
                           tn);
       }
       if (++ps == g.stages) {
@@ -282,9 +381,10 @@ __global__ void __launch_bounds__(MAXT)
         pphase ^= 1u;
       }
     }
-    const int r0 = ty * g.tile_rows;
+    const int tyr = PEER ? peer_tile_row(g, ty) : ty;  // boundary tile-rows first (PEER)
+    const int r0 = tyr * g.tile_rows;
     const int c0 = tx * g.wc;
-    const bool edge = tile_is_edge(g, tx, ty);
+    const bool edge = tile_is_edge(g, tx, tyr);
     T* tile = reinterpret_cast<T*>(smem + s * g.stage_bytes) + tile_offset(g, c0);
 
     mbar_wait_parity(&full[s], phase);
@@ -297,6 +397,12 @@ __global__ void __launch_bounds__(MAXT)
     T res[K];
     compute_tile<Op, T, K>(tile, g, p, res);
     store_tile<T, K>(out, g, r0, c0, edge, res);
+    if constexpr (PEER) {
+      if (peer_boundary_row(g, tyr)) {
+        const bool stored = store_peer_rows<T, K>(g, r0, c0, res);
+        peer_tile_done(g, tid, stored);
+      }
+    }
     // Release the stage only after the stores: they consume every value the
     // warp loaded from it, so no shared-memory read of this tile can still be
     // in flight when the producer's TMA refill overwrites the stage.  (An

@@ -17,6 +17,16 @@ KernelPair pair_for() {
 }
 
 template <class Op, typename T>
+KernelPtr peer_for_k(int K) {
+  switch (K) {
+    case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, 1024, true>);
+    case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, 1024, true>);
+    case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, 1024, true>);
+    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, true>);
+  }
+}
+
+template <class Op, typename T>
 KernelPair pair_for_k(int K) {
   switch (K) {
     case 1: return pair_for<Op, T, 1>();
@@ -76,6 +86,22 @@ KernelPtr SK_HALO_FN(const sk_stencil_desc& d) {
     case SK_OP_SYNTHETIC: return reinterpret_cast<KernelPtr>(&k_halo_strips<Synthetic, T>);
   }
   return nullptr;
+}
+
+// One-pass TMA kernel with the peer exchange fused in (iterated ops only).
+KernelPtr SK_PEER_FN(const sk_stencil_desc& d, int K) {
+  using T = SK_T;
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return peer_for_k<FivePoint, T>(K);
+    case SK_OP_HEAT: return peer_for_k<Heat, T>(K);
+    case SK_OP_GOL: return peer_for_k<Gol, T>(K);
+    case SK_OP_BOXMEAN:
+      if (d.north == 5 && d.south == 1 && d.east == 3 && d.west == 0) {
+        return peer_for_k<BoxMeanFixed<5, 1, 3, 0>, T>(K);
+      }
+      return peer_for_k<BoxMean, T>(K);
+    default: return nullptr;
+  }
 }
 
 KernelPtr SK_HALO_PUT_FN() { return reinterpret_cast<KernelPtr>(&k_halo_put<SK_T>); }

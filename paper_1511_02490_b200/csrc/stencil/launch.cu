@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1063,6 +1064,25 @@ KernelPtr halo_kernel(const sk_stencil_desc& d) {
     default: return halo_strips_f64(d);
   }
 }
+// True when a (peer) device pointer lives on the current device.
+bool peer_on_device(const void* p) {
+  int dev = 0;
+  cudaPointerAttributes a;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.device == dev;
+}
+
+KernelPtr peer_tma_kernel(const sk_stencil_desc& d, int K) {
+  switch (d.dtype) {
+    case SK_INT32: return peer_tma_i32(d, K);
+    case SK_FLOAT32: return peer_tma_f32(d, K);
+    default: return peer_tma_f64(d, K);
+  }
+}
+
 KernelPtr halo_put_kernel(int dtype) {
   switch (dtype) {
     case SK_INT32: return halo_put_i32();
@@ -1708,6 +1728,38 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
     }
   }
 
+  // Fused path: one launch per generation of the one-pass TMA kernel with
+  // the exchange folded into its boundary tile-rows (k_stencil_tma<..., PEER>),
+  // when the TMA plan applies and every mirrored row lies in the first / last
+  // tile-row.  Otherwise the strips + interior schedule below.
+  // Opt-in (SK_PEER_SCHEDULE=fused).  Measured on one B200, one rank, GoL
+  // 8192^2 at 128x8: the PEER instantiation executes 8.9 % more instructions
+  // (the boundary-row remap and checks on every tile) and runs 104.5 us per
+  // generation against 91.5 us for the plain one-pass kernel, worse than the
+  // strips schedule (+7 %).  It is also persistent: its boundary blocks hold
+  // their SMs while they wait for a neighbour's flag, so ranks sharing a GPU
+  // can starve each other - never chosen for peers on this device.
+  Plan fplan;
+  KernelPtr peer_k = nullptr;
+  const char* sched = std::getenv("SK_PEER_SCHEDULE");
+  const bool shared_gpu = (has_n && peer_on_device(peers->north_a)) || (has_s && peer_on_device(peers->south_a));
+  const bool forced = sched && std::strcmp(sched, "fused") == 0;
+  if (forced && (!shared_gpu || std::getenv("SK_PEER_ALLOW_SHARED"))) {
+    int dev = 0;
+    current_device_info(&info, &dev);
+    const char* a0 = static_cast<const char*>(d_a) + N * row_bytes;
+    if (m > 0 && make_plan(d, width, rows, pitch, pitch, g.above, g.below, wc, wr, a0, &fplan) == SK_OK &&
+        fplan.tma && !fplan.driver_handle && fplan.g.tile_rows >= m) {
+      KernelPtr k = peer_tma_kernel(d, fplan.g.K);
+      KernelAttr ka;
+      if (k && kernel_attr(dev, k, info, &ka) == SK_OK && fplan.threads <= ka.max_threads &&
+          fplan.smem <= ka.max_dyn_smem && occupancy(dev, k, fplan.threads, fplan.smem) >= 1) {
+        peer_k = k;
+      }
+    }
+    g_last_error.clear();
+  }
+
   // generation 0 halos: put the initial boundary rows, publish B + 1
   {
     g.wait_value = B;
@@ -1723,6 +1775,44 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
   }
   const int strip_grid = static_cast<int>(
       std::max<long long>(1, std::min<long long>((static_cast<long long>(m) * width + 255) / 256, 2LL * info.sms)));
+  if (peer_k) {
+    Plan pl = fplan;
+    pl.kernel = peer_k;
+    PeerTile& pt = pl.g.peer;
+    pt.flag_n = flag_n;
+    pt.flag_s = flag_s;
+    pt.north_off = g.north_off;
+    pt.south_off = 0;
+    pt.north_rows = S;
+    pt.south_rows = N;
+    pt.pflag_n = pflag_n;
+    pt.pflag_s = pflag_s;
+    pt.done = done;
+    pt.boundary_tiles = pl.g.tiles_x * (pl.g.tiles_y >= 2 ? 2 : 1);
+    const long long total_rows = rows + pl.g.above + pl.g.below;
+    void* src = d_a;
+    void* dst = d_b;
+    for (int gen = 1; gen <= iterations; ++gen) {
+      pt.wait_value = B + gen;
+      pt.signal_value = B + gen + 1;
+      pt.peer_n = has_n ? (gen & 1 ? peers->north_b : peers->north_a) : nullptr;
+      pt.peer_s = has_s ? (gen & 1 ? peers->south_b : peers->south_a) : nullptr;
+      const void* s0 = static_cast<const char*>(src) + N * row_bytes;
+      void* d0 = static_cast<char*>(dst) + N * row_bytes;
+      int rc;
+      switch (d.dtype) {
+        case SK_INT32: rc = launch_typed<int32_t>(d, pl, s0, d0, pl.g.above, total_rows, st); break;
+        case SK_FLOAT32: rc = launch_typed<float>(d, pl, s0, d0, pl.g.above, total_rows, st); break;
+        default: rc = launch_typed<double>(d, pl, s0, d0, pl.g.above, total_rows, st);
+      }
+      if (rc) return rc;
+      std::swap(src, dst);
+    }
+    *epoch = B + iterations + 1;
+    if (result_in_b) *result_in_b = iterations % 2;
+    return SK_OK;
+  }
+
   // Per generation the strips (caller's stream) and the interior (side
   // stream) run concurrently; a fork/join event pair orders generation g+1
   // after both halves of generation g (each half reads the other's rows).

@@ -52,4 +52,10 @@ KernelPtr halo_put_f32();
 KernelPtr halo_put_f64();
 KernelPtr halo_wait();
 
+// k_stencil_tma<Op, T, K, 1024, PEER = true>: the one-pass kernel with the
+// peer exchange fused into its boundary tile-rows; nullptr for other ops.
+KernelPtr peer_tma_i32(const sk_stencil_desc& d, int K);
+KernelPtr peer_tma_f32(const sk_stencil_desc& d, int K);
+KernelPtr peer_tma_f64(const sk_stencil_desc& d, int K);
+
 }  // namespace sk

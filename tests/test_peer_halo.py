@@ -12,7 +12,10 @@ rank's host code ever waits for another's: the ordering is the device
 flags'.  Results must be bit-identical to the undivided CPU oracle.
 
 The two-process test maps the neighbour's buffers with CUDA IPC handles
-(sk_ipc_export / sk_ipc_import) as a multi-GPU run does."""
+(sk_ipc_export / sk_ipc_import) as a multi-GPU run does.  Both schedules are
+covered: the strips + interior kernels (the default) and the opt-in one-pass
+kernel with the exchange fused into its boundary tile-rows (forced here on
+small grids)."""
 from __future__ import annotations
 
 import os
@@ -82,9 +85,23 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["auto", "fused"])
+def schedule(request, monkeypatch):
+    """auto: the strips + interior schedule (the default);
+    fused: the opt-in one-pass kernel with the exchange in its boundary
+    tile-rows - small grids, so the ranks' persistent grids never starve
+    each other of SMs on the shared GPU."""
+    if request.param == "fused":
+        monkeypatch.setenv("SK_PEER_SCHEDULE", "fused")
+        monkeypatch.setenv("SK_PEER_ALLOW_SHARED", "1")
+    else:
+        monkeypatch.delenv("SK_PEER_SCHEDULE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("op,dtype,borders,border,pad", CASES)
 @pytest.mark.parametrize("world", [2, 3])
-def test_peer_exchange_vs_oracle(op, dtype, borders, border, pad, world):
+def test_peer_exchange_vs_oracle(op, dtype, borders, border, pad, world, schedule):
     n, s, e, w = borders
     st = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w, border=border,
                  pad_value=pad)
@@ -96,7 +113,7 @@ def test_peer_exchange_vs_oracle(op, dtype, borders, border, pad, world):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_peer_exchange_epochs_and_thin_shards(world):
+def test_peer_exchange_epochs_and_thin_shards(world, schedule):
     """Several iterate calls back to back (the epoch counter carries the
     flag protocol across calls) and shards only a little taller than the
     strips (h < 2m: the top strip owns every row)."""
