@@ -78,8 +78,8 @@ def main() -> int:
     funcs = sass_functions(OBJ)
 
     def counts_for(op: str) -> dict[str, int]:
-        want = f"void sk::k_stencil_tma<sk::{op}, float, 8, 1024>"
-        hits = [n for n in funcs if n.startswith(want)]
+        want = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024(, false)?>\(")
+        hits = [n for n in funcs if want.match(n)]
         if len(hits) != 1:
             raise SystemExit(f"no unique SASS function for {want}: {hits[:3]}")
         return categorise(funcs[hits[0]])

@@ -5,6 +5,7 @@ sm_100a object.  CPU only (cuobjdump disassembles without a GPU)."""
 from __future__ import annotations
 
 import importlib.util
+import re
 import shutil
 from pathlib import Path
 
@@ -29,12 +30,14 @@ def test_categorise_bins_every_opcode_once():
 @pytest.mark.skipif(not shutil.which("cuobjdump") or not sf.OBJ.exists(), reason="needs cuobjdump + build")
 def test_executor_kernels_have_sass_features():
     funcs = sf.sass_functions(sf.OBJ)
-    for op in ("Heat", "Gol", "Sobel", "Synthetic"):
-        name = f"void sk::k_stencil_tma<sk::{op}, float, 8, 1024>"
-        hits = [n for n in funcs if n.startswith(name)]
+    def one(op):
+        want = re.compile(rf"void sk::k_stencil_tma<sk::{op}, float, 8, 1024(, false)?>\(")
+        hits = [n for n in funcs if want.match(n)]
         assert len(hits) == 1, op
-        c = sf.categorise(funcs[hits[0]])
+        return sf.categorise(funcs[hits[0]])
+
+    for op in ("Heat", "Gol", "Sobel", "Synthetic"):
+        c = one(op)
         assert sum(c.values()) > 100 and c["load"] > 0 and c["store"] > 0 and c["branch"] > 0
-    heat = sf.categorise(funcs[[n for n in funcs if n.startswith("void sk::k_stencil_tma<sk::Heat, float, 8")][0]])
-    gol = sf.categorise(funcs[[n for n in funcs if n.startswith("void sk::k_stencil_tma<sk::Gol, float, 8")][0]])
+    heat, gol = one("Heat"), one("Gol")
     assert heat["float_arith"] > gol["float_arith"]  # heat is FP work, gol counts integers
