@@ -8,34 +8,18 @@
 //   refused    <=> the staged tile does not fit the opt-in shared memory, no
 //                  block can be resident, or the launch reports a
 //                  (non-sticky) configuration/resource error.
-#include <cuda.h>
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
 #include <cstdarg>
+#include <cmath>
 #include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <map>
-#include <mutex>
 #include <random>
-#include <string>
 #include <thread>
-#include <tuple>
-#include <vector>
 
-#include "cross_strips.cuh"
-#include "gol_bits.cuh"
-#include "halo.cuh"
-#include "kernels.cuh"
-#include "registry.cuh"
-#include "sk_stencil.h"
+#include "launch_internal.cuh"
 
 namespace sk {
-namespace {
+namespace detail {
 
-thread_local std::string g_last_error;
+thread_local std::string g_last_error;  // declared in launch_internal.cuh
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -57,18 +41,10 @@ bool is_config_error(cudaError_t e) {
 
 size_t dtype_size(int dtype) { return dtype == SK_FLOAT64 ? 8 : 4; }
 
-struct DeviceInfo {
-  int sms = 0;
-  int max_threads = 0;
-  int smem_optin = 0;
-  int smem_per_sm = 0;
-  int l2_bytes = 0;
-};
-
 std::mutex g_mu;
 std::map<int, DeviceInfo> g_devices;
 
-int current_device_info(DeviceInfo* out, int* dev_out = nullptr) {
+int current_device_info(DeviceInfo* out, int* dev_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(SK_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
@@ -109,40 +85,7 @@ int cells_per_thread(const sk_stencil_desc& d, int wr, long long H) {
 }
 
 // ------------------------------------------------------------ op parameters
-long long binom(int n, int k) {
-  long long r = 1;
-  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
-  return r;
-}
-
-template <typename T>
-void fill_params(const sk_stencil_desc& d, OpParams<T>* p) {
-  std::memset(p, 0, sizeof(*p));
-  p->north = d.north;
-  p->south = d.south;
-  p->east = d.east;
-  p->west = d.west;
-  p->complexity = d.complexity;
-  // Synthetic kernels: instruction budget -> dependent ALU steps per cell
-  // (DESIGN.md §3.9): heavy (synthetic-b) instructions/4, light instructions/32.
-  p->alu_iters = d.op == SK_OP_SYNTHETIC ? (d.complexity ? d.instructions / 4 : d.instructions / 32)
-                                         : 0;
-  if (d.op == SK_OP_GAUSSIAN) {
-    const int g = d.north;
-    p->gauss_radius = g;
-    for (int j = 0; j <= 2 * g; ++j) {
-      const long long c = binom(2 * g, j);
-      if constexpr (std::is_same_v<T, int32_t>) {
-        p->gauss_b[j] = c;
-      } else {
-        p->gauss_b[j] = static_cast<T>(std::ldexp(static_cast<double>(c), -2 * g));
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------- descriptor checks
-constexpr int kMaxBitsTB = 128;
 
 // Game of Life takes the bit-plane kernel when asked to, or under AUTO once
 // generations are fused - unless the descriptor asks for a per-cell work-item
@@ -160,7 +103,6 @@ bool uses_bits(const sk_stencil_desc& d) {
 
 // five_point / heat with unit borders take the register-strip kernel when
 // asked to, or under AUTO for TB > 4 (beyond the per-cell fused kernel).
-constexpr int kMaxStripsTB = 32;
 bool uses_strips(const sk_stencil_desc& d) {
   if (d.op != SK_OP_FIVE_POINT && d.op != SK_OP_HEAT) return false;
   if (d.north != 1 || d.south != 1 || d.east != 1 || d.west != 1) return false;
@@ -286,16 +228,12 @@ const DriverApi& driver() {
 
 // Per-(device, kernel) attributes: kernel max threads and the opt-in smem
 // attribute, set once.
-struct KernelAttr {
-  int max_threads = 0;
-  int max_dyn_smem = 0;
-};
 std::map<std::pair<int, KernelPtr>, KernelAttr> g_kattr;
 
 
 
 int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out,
-                bool is_driver = false) {
+                bool is_driver) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_pair(dev, k);
   auto it = g_kattr.find(key);
@@ -338,7 +276,7 @@ int kernel_attr(int dev, KernelPtr k, const DeviceInfo& info, KernelAttr* out,
 
 std::map<std::tuple<int, KernelPtr, int, int>, int> g_occ;
 
-int occupancy(int dev, KernelPtr k, int threads, int smem, bool is_driver = false) {
+int occupancy(int dev, KernelPtr k, int threads, int smem, bool is_driver) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_occ.find({dev, k, threads, smem});
@@ -378,17 +316,6 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-struct MapKey {
-  int dev;
-  const void* base;
-  int dtype;
-  long long w, h, pitch;
-  int box_w, box_h;
-  bool operator<(const MapKey& o) const {
-    return std::tie(dev, base, dtype, w, h, pitch, box_w, box_h) <
-           std::tie(o.dev, o.base, o.dtype, o.w, o.h, o.pitch, o.box_w, o.box_h);
-  }
-};
 std::map<MapKey, CUtensorMap> g_maps;
 
 int tensor_map(const MapKey& key, CUtensorMap* out) {
@@ -422,25 +349,13 @@ int tensor_map(const MapKey& key, CUtensorMap* out) {
 }
 
 // ------------------------------------------------------------------ plan
-struct Plan {
-  Geom g{};
-  KernelPtr kernel = nullptr;
-  bool driver_handle = false;  // kernel is a CUfunction of a custom functor
-  bool tma = false;
-  int threads = 0;
-  int smem = 0;
-  int grid = 0;
-  int kernel_max = 0;
-  long long tile_bytes = 0;
-};
-
 // Builds the launch plan; returns SK_OK, SK_OVERSIZED, SK_REFUSED or an error.
 // `in` may be null for a probe (TMA eligibility then assumes aligned buffers).
 int k_index(int K) { return K == 1 ? 0 : K == 2 ? 1 : K == 4 ? 2 : 3; }
 
 int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
               long long pitch_out, long long above, long long below, int wc, int wr,
-              const void* in, Plan* plan, const sk_kernel_table* custom = nullptr) {
+              const void* in, Plan* plan, const sk_kernel_table* custom) {
   if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) {
     return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
   }
@@ -602,135 +517,6 @@ int launch_driver(const Plan& plan, dim3 grid, dim3 block, void** args, cudaStre
   return fail(SK_ECUDA, "custom kernel launch failed (driver error %d)", static_cast<int>(r));
 }
 
-template <typename T>
-int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* in, void* out,
-                 long long above_rows, long long H_total_rows, cudaStream_t stream) {
-  OpParams<T> p;
-  fill_params<T>(d, &p);
-  T pad = static_cast<T>(d.pad_value);
-  dim3 block(plan.g.wc, plan.g.wr, 1);
-  cudaError_t e;
-  if (plan.tma) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    MapKey key{dev,
-               static_cast<const char*>(in) -
-                   above_rows * plan.g.pitch_in * static_cast<long long>(sizeof(T)),
-               d.dtype,
-               plan.g.W,
-               H_total_rows,
-               plan.g.pitch_in,
-               plan.g.tile_w,
-               plan.g.box_h};
-    CUtensorMap map;
-    if (int rc = tensor_map(key, &map)) return rc;
-    void* args[] = {&map, &out, const_cast<Geom*>(&plan.g), &pad, &p};
-    if (plan.driver_handle) return launch_driver(plan, dim3(plan.grid), block, args, stream);
-    e = cudaLaunchKernel(plan.kernel, dim3(plan.grid), block, args, plan.smem, stream);
-  } else {
-    const T* tin = static_cast<const T*>(in);
-    T* tout = static_cast<T*>(out);
-    void* args[] = {&tin, &tout, const_cast<Geom*>(&plan.g), &pad, &p};
-    if (plan.driver_handle) {
-      return launch_driver(plan, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args, stream);
-    }
-    e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args,
-                         plan.smem, stream);
-  }
-  if (e != cudaSuccess) {
-    if (is_config_error(e)) {
-      cudaGetLastError();
-      return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
-    }
-    return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
-  }
-  return SK_OK;
-}
-
-// ------------------------------------------------------- bit-plane (gol)
-KernelPtr pack_kernel(int dtype) {
-  switch (dtype) {
-    case SK_INT32: return gol_pack_i32();
-    case SK_FLOAT32: return gol_pack_f32();
-    default: return gol_pack_f64();
-  }
-}
-KernelPtr unpack_kernel(int dtype) {
-  switch (dtype) {
-    case SK_INT32: return gol_unpack_i32();
-    case SK_FLOAT32: return gol_unpack_f32();
-    default: return gol_unpack_f64();
-  }
-}
-
-// Rows per lane of the strip kernel: the descriptor's K in {8, 16, 32}, or 16.
-int strip_rows(const sk_stencil_desc& d) { return d.cells_per_thread > 0 ? d.cells_per_thread : 16; }
-
-struct StripPlan {
-  StripGeom g{};
-  KernelPtr kernel = nullptr;
-  int threads = 0;     // launched: wc*wr rounded up to whole warps
-  int smem = 0;
-  long long grid = 0;
-  int kernel_max = 0;
-  long long tile_bytes = 0;
-};
-
-// Legality and geometry of one k_gol_strips launch advancing `tb`
-// generations of a packed W x H grid whose readable rows are [lo, hi].
-int make_strips_plan(const sk_stencil_desc& d, long long W, long long H, long long lo,
-                     long long hi, int wc, int wr, int tb, StripPlan* plan) {
-  if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
-  if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
-  if (tb < 1 || tb > kMaxBitsTB) return fail(SK_EINVAL, "bad generation count %d", tb);
-  DeviceInfo info;
-  int dev = 0;
-  if (int rc = current_device_info(&info, &dev)) return rc;
-  const int R = strip_rows(d);
-  plan->kernel = gol_strips(R);
-  if (!plan->kernel) return fail(SK_EINVAL, "bit-plane rows per work-item must be 8, 16 or 32");
-  KernelAttr attr;
-  if (int rc = kernel_attr(dev, plan->kernel, info, &attr)) return rc;
-  plan->kernel_max = std::min(info.max_threads, attr.max_threads);
-  const long long threads = static_cast<long long>(wc) * wr;
-  if (threads > plan->kernel_max) {
-    return fail(SK_OVERSIZED, "workgroup %dx%d exceeds the effective maximum %d", wc, wr,
-                plan->kernel_max);
-  }
-  plan->threads = static_cast<int>((threads + 31) / 32 * 32);
-  const int nwarps = plan->threads / 32;
-  StripGeom& g = plan->g;
-  g.W = static_cast<int>(W);
-  g.H = static_cast<int>(H);
-  g.lo = static_cast<int>(lo);
-  g.hi = static_cast<int>(hi);
-  g.nwords = static_cast<int>((W + 31) / 32);
-  g.tb = tb;
-  g.hw = (tb + 31) / 32;
-  g.ow = 32 - 2 * g.hw;
-  g.th = nwarps * R - 2 * tb;
-  if (g.th < 1 || g.ow < 1) {
-    return fail(SK_REFUSED, "a %d-row x 32-word tile cannot hold %d halo generations", nwarps * R, tb);
-  }
-  g.tiles_x = (g.nwords + g.ow - 1) / g.ow;
-  g.tiles_y = static_cast<int>((H + g.th - 1) / g.th);
-  g.mode = d.border_mode;
-  const double padv = d.pad_value;
-  const bool pad_alive = d.dtype == SK_INT32 ? static_cast<int32_t>(padv) != 0
-                         : d.dtype == SK_FLOAT32 ? static_cast<float>(padv) != 0.0f
-                                                 : padv != 0.0;
-  g.padword = pad_alive ? 0xffffffffu : 0u;
-  plan->tile_bytes = static_cast<long long>(nwarps) * R * 32 * 4;  // bit tile in registers
-  plan->smem = (2 * nwarps * 64 + 64) * 4;
-  if (plan->smem > attr.max_dyn_smem) return fail(SK_REFUSED, "exchange area exceeds shared memory");
-  if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
-    return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
-  }
-  plan->grid = static_cast<long long>(g.tiles_x) * g.tiles_y;
-  if (plan->grid >= (1LL << 31)) return fail(SK_REFUSED, "grid of %lld tiles too large", plan->grid);
-  return SK_OK;
-}
-
 int launch_checked(KernelPtr k, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
   cudaError_t e = cudaLaunchKernel(k, grid, block, args, smem, stream);
   if (e == cudaSuccess) return SK_OK;
@@ -741,184 +527,9 @@ int launch_checked(KernelPtr k, dim3 grid, dim3 block, void** args, int smem, cu
   return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
 }
 
-int scratch_bits(long long words, void** p0, void** p1);  // below (per-thread scratch)
-
-// `iterations` generations of gol on the bit-plane path: pack (T -> bits,
-// rows [-above, H + below) when the generations fit one launch), then
-// ceil(iterations / TB) strip launches ping-ponging two packed grids, then
-// unpack into `out`.  Halo rows are only meaningful for a single launch
-// (iterations <= TB), as for sk_stencil_launch on a row shard.
-int run_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
-             long long pitch_in, long long pitch_out, long long above, long long below, int wc,
-             int wr, int iterations, int TB, cudaStream_t stream) {
-  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
-  TB = std::max(1, TB);
-  const long long a = iterations <= TB ? std::min<long long>(above, iterations) : 0;
-  const long long b = iterations <= TB ? std::min<long long>(below, iterations) : 0;
-  StripPlan first;
-  if (int rc = make_strips_plan(d, W, H, -a, H - 1 + b, wc, wr, std::max(1, std::min(TB, iterations)),
-                                &first)) {
-    return rc;
-  }
-  if (iterations == 0) return SK_OK;
-  const long long pw = (first.g.nwords + 3) / 4 * 4;  // 16-B packed rows
-  void* P[2] = {nullptr, nullptr};
-  if (int rc = scratch_bits(pw * (H + a + b), &P[0], &P[1])) return rc;
-  DeviceInfo info;
-  if (int rc = current_device_info(&info)) return rc;
-  const int cvt_grid = 4 * info.sms * 8;  // 8 warps per block, grid-stride
-  {  // pack rows [-a, H + b) of `in` into P[0]
-    const void* base = static_cast<const char*>(in) - a * pitch_in * static_cast<long long>(dtype_size(d.dtype));
-    int row0 = 0, rows = static_cast<int>(H + a + b), w = static_cast<int>(W);
-    long long pi = pitch_in, pwl = pw;
-    void* args[] = {&base, &pi, &row0, &rows, &w, &P[0], &pwl};
-    if (int rc = launch_checked(pack_kernel(d.dtype), dim3(cvt_grid), dim3(256), args, 0, stream)) return rc;
-  }
-  int cur = 0, done = 0;
-  for (bool firstl = true; done < iterations; firstl = false) {
-    const int tb = std::min(TB, iterations - done);
-    StripPlan plan;
-    if (int rc = make_strips_plan(d, W, H, firstl ? -a : 0, firstl ? H - 1 + b : H - 1, wc, wr, tb, &plan)) {
-      return rc;
-    }
-    plan.g.pw_in = pw;
-    plan.g.pw_out = pw;
-    const uint32_t* src = static_cast<const uint32_t*>(P[cur]) + (firstl ? a * pw : 0);
-    uint32_t* dst = static_cast<uint32_t*>(P[1 - cur]);
-    void* args[] = {&src, &dst, &plan.g};
-    if (int rc = launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads),
-                                args, plan.smem, stream)) {
-      return rc;
-    }
-    cur = 1 - cur;
-    done += tb;
-  }
-  {  // unpack P[cur] rows [0, H) into `out`
-    const void* src = P[cur];
-    long long pwl = pw, po = pitch_out;
-    int rows = static_cast<int>(H), w = static_cast<int>(W);
-    int vec = (pitch_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    void* args[] = {&src, &pwl, &rows, &w, &out, &po, &vec};
-    if (int rc = launch_checked(unpack_kernel(d.dtype), dim3(cvt_grid), dim3(256), args, 0, stream)) return rc;
-  }
-  return SK_OK;
-}
-
-// ------------------------------------------- register strips (cross ops)
-KernelPtr cross_kernel(const sk_stencil_desc& d, int R) {
-  switch (d.dtype) {
-    case SK_INT32: return cross_strips_i32(d, R);
-    case SK_FLOAT32: return cross_strips_f32(d, R);
-    default: return cross_strips_f64(d, R);
-  }
-}
-
-// Rows per lane of the cross-strip kernel: the descriptor's K in {4, 8, 16},
-// or 8 (4 for float64, whose 8-row strips spill) - two resident blocks per SM.
-int cross_rows(const sk_stencil_desc& d) {
-  return d.cells_per_thread > 0 ? d.cells_per_thread : (d.dtype == SK_FLOAT64 ? 4 : 8);
-}
-
-struct CrossPlan {
-  CrossGeom g{};
-  KernelPtr kernel = nullptr;
-  int threads = 0;
-  int smem = 0;
-  long long grid = 0;
-  int kernel_max = 0;
-  long long tile_bytes = 0;
-};
-
-// Legality and geometry of one k_cross_strips launch advancing `tb`
-// generations of a W x H region whose readable input rows are [lo, hi].
-int make_cross_plan(const sk_stencil_desc& d, long long W, long long H, long long pitch_in,
-                    long long pitch_out, long long lo, long long hi, int wc, int wr, int tb,
-                    const void* in, const void* out, CrossPlan* plan) {
-  if (W < 1 || H < 1 || W > (1LL << 30) || H > (1LL << 30)) return fail(SK_EINVAL, "bad dims %lldx%lld", W, H);
-  if (pitch_in < W || pitch_out < W) return fail(SK_EINVAL, "pitch smaller than width");
-  if (wc < 1 || wr < 1) return fail(SK_EINVAL, "bad workgroup %dx%d", wc, wr);
-  if (tb < 1 || tb > kMaxStripsTB) return fail(SK_EINVAL, "bad generation count %d", tb);
-  DeviceInfo info;
-  int dev = 0;
-  if (int rc = current_device_info(&info, &dev)) return rc;
-  const int R = cross_rows(d);
-  plan->kernel = cross_kernel(d, R);
-  if (!plan->kernel) return fail(SK_EINVAL, "register-strip rows per work-item must be 4, 8 or 16");
-  KernelAttr attr;
-  if (int rc = kernel_attr(dev, plan->kernel, info, &attr)) return rc;
-  plan->kernel_max = std::min(info.max_threads, attr.max_threads);
-  const long long threads = static_cast<long long>(wc) * wr;
-  if (threads > plan->kernel_max) {
-    return fail(SK_OVERSIZED, "workgroup %dx%d exceeds the effective maximum %d", wc, wr,
-                plan->kernel_max);
-  }
-  plan->threads = static_cast<int>((threads + 31) / 32 * 32);
-  const int nwarps = plan->threads / 32;
-  CrossGeom& g = plan->g;
-  g.pitch_in = pitch_in;
-  g.pitch_out = pitch_out;
-  g.W = static_cast<int>(W);
-  g.H = static_cast<int>(H);
-  g.lo = static_cast<int>(lo);
-  g.hi = static_cast<int>(hi);
-  g.tb = tb;
-  g.hl = (tb + 3) / 4;
-  g.oc = 4 * (32 - 2 * g.hl);
-  g.th = nwarps * R - 2 * tb;
-  if (g.th < 1 || g.oc < 4) {
-    return fail(SK_REFUSED, "a %d-row x 128-column tile cannot hold %d halo generations", nwarps * R, tb);
-  }
-  g.tiles_x = static_cast<int>((W + g.oc - 1) / g.oc);
-  g.tiles_y = static_cast<int>((H + g.th - 1) / g.th);
-  g.mode = d.border_mode;
-  const size_t es = dtype_size(d.dtype);
-  g.vec = (pitch_in % 4 == 0) && (pitch_out % 4 == 0) &&
-          (reinterpret_cast<uintptr_t>(in) % (4 * es) == 0) &&
-          (reinterpret_cast<uintptr_t>(out) % (4 * es) == 0);
-  plan->tile_bytes = static_cast<long long>(nwarps) * R * 128 * static_cast<long long>(es);  // in registers
-  plan->smem = static_cast<int>(2 * nwarps * 64 * 4 * es);
-  if (plan->smem > attr.max_dyn_smem) return fail(SK_REFUSED, "exchange area exceeds shared memory");
-  if (occupancy(dev, plan->kernel, plan->threads, plan->smem) < 1) {
-    return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
-  }
-  plan->grid = static_cast<long long>(g.tiles_x) * g.tiles_y;
-  if (plan->grid >= (1LL << 31)) return fail(SK_REFUSED, "grid of %lld tiles too large", plan->grid);
-  return SK_OK;
-}
-
-template <typename T>
-int launch_cross_typed(const sk_stencil_desc& d, const CrossPlan& plan, const void* in, void* out,
-                       cudaStream_t stream) {
-  OpParams<T> p;
-  fill_params<T>(d, &p);
-  T pad = static_cast<T>(d.pad_value);
-  const T* tin = static_cast<const T*>(in);
-  T* tout = static_cast<T*>(out);
-  void* args[] = {&tin, &tout, const_cast<CrossGeom*>(&plan.g), &pad, &p};
-  return launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads), args,
-                        plan.smem, stream);
-}
-
-// One k_cross_strips launch: `tb` generations from `in` (row 0 of the region,
-// `above` / `below` readable halo rows) into `out`.
-int run_cross(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
-              long long pitch_in, long long pitch_out, long long above, long long below, int wc,
-              int wr, int tb, cudaStream_t stream) {
-  CrossPlan plan;
-  if (int rc = make_cross_plan(d, W, H, pitch_in, pitch_out, -above, H - 1 + below, wc, wr, tb, in,
-                               out, &plan)) {
-    return rc;
-  }
-  switch (d.dtype) {
-    case SK_INT32: return launch_cross_typed<int32_t>(d, plan, in, out, stream);
-    case SK_FLOAT32: return launch_cross_typed<float>(d, plan, in, out, stream);
-    default: return launch_cross_typed<double>(d, plan, in, out, stream);
-  }
-}
-
 int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,
            long long pitch_in, long long pitch_out, long long above, long long below, int wc,
-           int wr, cudaStream_t stream, const sk_kernel_table* custom = nullptr) {
+           int wr, cudaStream_t stream, const sk_kernel_table* custom) {
   if (!custom && uses_strips(d)) {
     return run_cross(d, in, out, W, H, pitch_in, pitch_out, above, below, wc, wr,
                      std::max(1, d.fused_iterations), stream);
@@ -996,33 +607,6 @@ int scratch(Scratch** out) {
   return SK_OK;
 }
 
-// Fork/join lane of a caller's stream for the peer schedule: the interior
-// launch of a generation runs on `side` while the caller's stream runs the
-// boundary strips (which may wait on a neighbour's flag).  Keyed by (device,
-// caller stream): ranks sharing a process each bring their own stream, and
-// one shared side stream would serialise their interiors into a cycle.
-struct SideLane {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-std::map<std::pair<int, cudaStream_t>, SideLane> g_side;
-
-int side_lane(cudaStream_t st, SideLane** out) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SK_ECUDA, "cudaGetDevice failed");
-  std::lock_guard<std::mutex> lk(g_mu);
-  SideLane& l = g_side[{dev, st}];
-  if (!l.side) {
-    if (cudaStreamCreateWithFlags(&l.side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming) != cudaSuccess) {
-      return fail(SK_ECUDA, "side stream/event creation failed");
-    }
-  }
-  *out = &l;
-  return SK_OK;
-}
-
 // Packed ping-pong grids of the bit-plane path (per device and thread, kept
 // and grown as needed; freed with the process).
 int scratch_bits(long long words, void** p0, void** p1) {
@@ -1056,177 +640,12 @@ __global__ void k_count_diff(const uint4* __restrict__ a, const uint4* __restric
   if (local) atomicAdd(diff, local);
 }
 
-// ------------------------------------------- peer-memory halo exchange
-KernelPtr halo_kernel(const sk_stencil_desc& d) {
-  switch (d.dtype) {
-    case SK_INT32: return halo_strips_i32(d);
-    case SK_FLOAT32: return halo_strips_f32(d);
-    default: return halo_strips_f64(d);
-  }
-}
-// True when a (peer) device pointer lives on the current device.
-bool peer_on_device(const void* p) {
-  int dev = 0;
-  cudaPointerAttributes a;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.device == dev;
-}
-
-KernelPtr peer_tma_kernel(const sk_stencil_desc& d, int K) {
-  switch (d.dtype) {
-    case SK_INT32: return peer_tma_i32(d, K);
-    case SK_FLOAT32: return peer_tma_f32(d, K);
-    default: return peer_tma_f64(d, K);
-  }
-}
-
-KernelPtr halo_put_kernel(int dtype) {
-  switch (dtype) {
-    case SK_INT32: return halo_put_i32();
-    case SK_FLOAT32: return halo_put_f32();
-    default: return halo_put_f64();
-  }
-}
-
-template <typename T>
-int launch_halo_strips(const sk_stencil_desc& d, const void* src, void* dst, void* peer_n,
-                       void* peer_s, const long long* flag_n, const long long* flag_s,
-                       long long* pflag_n, long long* pflag_s, unsigned* done, const HaloGeom& g,
-                       int grid_x, cudaStream_t stream) {
-  OpParams<T> p;
-  fill_params<T>(d, &p);
-  T pad = static_cast<T>(d.pad_value);
-  void* args[] = {const_cast<void**>(&src), &dst, &peer_n, &peer_s, const_cast<long long**>(&flag_n),
-                  const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done,
-                  const_cast<HaloGeom*>(&g), &pad, &p};
-  return launch_checked(halo_kernel(d), dim3(grid_x, 2), dim3(256), args, 0, stream);
-}
-
-// Temporally blocked peer schedule (register-strip path, TB generations per
-// exchange).  The shard buffers carry TB-deep halos: TB*N rows above, TB*S
-// below.  Per launch k (generations (k-1)TB+1 .. kTB, the last one shorter):
-//   k_halo_wait   acquire the neighbours' state-(k-1) halos (value B + k);
-//   strips        k_cross_strips over the top / bottom m = TB*max(N,S) rows;
-//   k_halo_put    their first TB*S / last TB*N rows into the neighbours' halos,
-//                 publish B + k + 1 (last block, release.sys);
-//   interior      k_cross_strips over rows [m, rows - m), owned rows only.
-// Same one-flag-per-direction argument as the one-generation schedule: the
-// neighbour publishes state k only after its launch-k strip pass - the last
-// reader of the halo rows overwritten by launch k+1's put - has run.
-int iterate_peer_strips(const sk_stencil_desc& d, void* d_a, void* d_b, int64_t width, int64_t rows,
-                        int64_t pitch, int32_t iterations, int32_t wc, int32_t wr,
-                        const sk_halo_peers& peers, void* d_control, int64_t* epoch,
-                        cudaStream_t st, int32_t* result_in_b) {
-  const int TB = d.fused_iterations;
-  const int Nh = TB * d.north, Sh = TB * d.south;
-  const int m = std::max(Nh, Sh);
-  if (width < 1 || pitch < width || rows < 2LL * m + std::max(Nh, Sh)) {
-    return fail(SK_EINVAL, "shard of %lld rows cannot hold %d-generation strips of %d rows",
-                (long long)rows, TB, m);
-  }
-  if ((peers.north_a == nullptr) != (peers.north_b == nullptr) ||
-      (peers.north_a == nullptr) != (peers.north_control == nullptr) ||
-      (peers.south_a == nullptr) != (peers.south_b == nullptr) ||
-      (peers.south_a == nullptr) != (peers.south_control == nullptr)) {
-    return fail(SK_EINVAL, "incomplete peer mapping");
-  }
-  const bool has_n = peers.north_a != nullptr, has_s = peers.south_a != nullptr;
-  if (has_n && peers.north_rows < 2LL * m) return fail(SK_EINVAL, "bad north_rows");
-  const size_t es = dtype_size(d.dtype);
-  const long long row_bytes = pitch * static_cast<long long>(es);
-  long long* ctl = static_cast<long long*>(d_control);
-  const long long* flag_n = has_n ? ctl + 0 : nullptr;
-  const long long* flag_s = has_s ? ctl + 1 : nullptr;
-  unsigned* done = reinterpret_cast<unsigned*>(ctl + 2);
-  long long* pflag_n = has_n ? static_cast<long long*>(peers.north_control) + 1 : nullptr;
-  long long* pflag_s = has_s ? static_cast<long long*>(peers.south_control) + 0 : nullptr;
-  DeviceInfo info;
-  int dev = 0;
-  if (int rc = current_device_info(&info, &dev)) return rc;
-
-  HaloGeom g{};
-  g.pitch = pitch;
-  g.W = static_cast<int>(width);
-  g.h = static_cast<int>(rows);
-  g.north_rows = Sh;
-  g.south_rows = Nh;
-  g.north_off = has_n ? (Nh + peers.north_rows) * pitch : 0;
-  g.south_off = 0;
-  g.mode = d.border_mode;
-  const long long B = *epoch;
-  const long long inner = rows - 2LL * m;
-
-  // Resolve every kernel before the first launch (lazy loading; see the
-  // one-generation schedule).
-  {
-    KernelAttr ka;
-    if (int rc = kernel_attr(dev, halo_wait(), info, &ka)) return rc;
-    if (int rc = kernel_attr(dev, halo_put_kernel(d.dtype), info, &ka)) return rc;
-    CrossPlan cp;
-    const char* a0 = static_cast<const char*>(d_a) + Nh * row_bytes;
-    if (int rc = make_cross_plan(d, width, m, pitch, pitch, -Nh, m - 1 + Sh, wc, wr, TB, a0, a0, &cp)) return rc;
-    if (int rc = make_cross_plan(d, width, inner, pitch, pitch, -Nh, inner - 1 + Sh, wc, wr, TB, a0, a0, &cp)) {
-      return rc;
-    }
-  }
-  const int put_grid = static_cast<int>(std::max<long long>(
-      1, std::min<long long>((static_cast<long long>(Nh + Sh) * width + 255) / 256, 4LL * info.sms)));
-  auto put = [&](const void* src_rows, void* pn, void* ps, long long wait, long long signal) {
-    g.wait_value = wait;
-    g.signal_value = signal;
-    void* args[] = {const_cast<void**>(&src_rows), &pn, &ps, const_cast<long long**>(&flag_n),
-                    const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done, &g};
-    return launch_checked(halo_put_kernel(d.dtype), dim3(put_grid), dim3(256), args, 0, st);
-  };
-  // state-0 halos
-  if (int rc = put(static_cast<const char*>(d_a) + Nh * row_bytes, peers.north_a, peers.south_a, B, B + 1)) {
-    return rc;
-  }
-  void* src = d_a;
-  void* dst = d_b;
-  int launches = 0;
-  for (int done_gens = 0; done_gens < iterations; ++launches) {
-    const int tb = std::min(TB, iterations - done_gens);
-    const long long k = launches + 1;
-    {
-      long long value = B + k;
-      void* args[] = {const_cast<long long**>(&flag_n), const_cast<long long**>(&flag_s), &value};
-      if (int rc = launch_checked(halo_wait(), dim3(1), dim3(32), args, 0, st)) return rc;
-    }
-    const char* s0 = static_cast<const char*>(src) + Nh * row_bytes;
-    char* d0 = static_cast<char*>(dst) + Nh * row_bytes;
-    // top strip: reads the north halo (if any) and TB*S owned rows below it
-    if (int rc = run_cross(d, s0, d0, width, m, pitch, pitch, has_n ? Nh : 0, Sh, wc, wr, tb, st)) return rc;
-    // bottom strip
-    if (int rc = run_cross(d, s0 + (rows - m) * row_bytes, d0 + (rows - m) * row_bytes, width, m, pitch,
-                           pitch, Nh, has_s ? Sh : 0, wc, wr, tb, st)) {
-      return rc;
-    }
-    void* pn = has_n ? (k & 1 ? peers.north_b : peers.north_a) : nullptr;
-    void* ps = has_s ? (k & 1 ? peers.south_b : peers.south_a) : nullptr;
-    if (int rc = put(d0, pn, ps, B + k, B + k + 1)) return rc;
-    if (inner > 0) {
-      if (int rc = run_cross(d, s0 + m * row_bytes, d0 + m * row_bytes, width, inner, pitch, pitch, Nh, Sh,
-                             wc, wr, tb, st)) {
-        return rc;
-      }
-    }
-    done_gens += tb;
-    std::swap(src, dst);
-  }
-  *epoch = B + launches + 1;
-  if (result_in_b) *result_in_b = launches % 2;
-  return SK_OK;
-}
-
-}  // namespace
+}  // namespace detail
 }  // namespace sk
 
 // ======================================================================= ABI
 using namespace sk;
+using namespace sk::detail;
 
 extern "C" {
 
@@ -1589,282 +1008,6 @@ int sk_fill_host(int32_t dtype, int32_t kind, uint64_t seed, void* h_out, int64_
       default: return fail(SK_EINVAL, "bad dtype");
     }
   }
-  return SK_OK;
-}
-
-int sk_ipc_export(const void* d_ptr, sk_ipc_handle* out) {
-  g_last_error.clear();
-  if (!d_ptr || !out) return fail(SK_EINVAL, "null argument");
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static GetRange get_range = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess) {
-      cudaGetLastError();
-      return static_cast<GetRange>(nullptr);
-    }
-    return reinterpret_cast<GetRange>(fn);
-  }();
-  if (!get_range) return fail(SK_ECUDA, "cuMemGetAddressRange unavailable");
-  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
-    return fail(SK_EINVAL, "pointer is not device memory");
-  }
-  cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
-  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
-  static_assert(sizeof(h) <= sizeof(out->handle), "IPC handle size");
-  std::memset(out, 0, sizeof(*out));
-  std::memcpy(out->handle, &h, sizeof(h));
-  out->offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
-  return SK_OK;
-}
-
-int sk_ipc_import(const sk_ipc_handle* h, void** d_ptr) {
-  g_last_error.clear();
-  if (!h || !d_ptr) return fail(SK_EINVAL, "null argument");
-  cudaIpcMemHandle_t mh;
-  std::memcpy(&mh, h->handle, sizeof(mh));
-  void* base = nullptr;
-  cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
-  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-  *d_ptr = static_cast<char*>(base) + h->offset;
-  return SK_OK;
-}
-
-int sk_ipc_close(void* d_ptr) {
-  g_last_error.clear();
-  // cudaIpcCloseMemHandle takes the mapped base; imported pointers carry an
-  // offset, so resolve the containing mapping first.
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-      q != cudaDriverEntryPointSuccess ||
-      reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
-    cudaGetLastError();
-    return fail(SK_EINVAL, "pointer is not a mapped device allocation");
-  }
-  cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
-  if (e != cudaSuccess) return fail(SK_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
-  return SK_OK;
-}
-
-int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
-                            int64_t rows, int64_t pitch, int32_t iterations, int32_t wc,
-                            int32_t wr, const sk_halo_peers* peers, void* d_control,
-                            int64_t* epoch, void* stream, int32_t* result_in_b) {
-  g_last_error.clear();
-  if (int rc = validate_desc(desc)) return rc;
-  const sk_stencil_desc& d = *desc;
-  if (!d_a || !d_b || !peers || !d_control || !epoch) return fail(SK_EINVAL, "null argument");
-  if (iterations < 0) return fail(SK_EINVAL, "negative iterations");
-  if (uses_strips(d) && d.fused_iterations > 1) {
-    return iterate_peer_strips(d, d_a, d_b, width, rows, pitch, iterations, wc, wr, *peers,
-                               d_control, epoch, static_cast<cudaStream_t>(stream), result_in_b);
-  }
-  if (d.fused_iterations > 1 || uses_bits(d) || uses_strips(d)) {
-    return fail(SK_ENOTSUP, "the peer-exchange schedule fuses generations only on the register-strip path");
-  }
-  const int N = d.north, S = d.south;
-  const int m = std::max(N, S);
-  if (width < 1 || pitch < width || rows < std::max(m, 1)) {
-    return fail(SK_EINVAL, "shard of %lld rows cannot hold halos of N=%d, S=%d", (long long)rows, N, S);
-  }
-  if ((peers->north_a == nullptr) != (peers->north_b == nullptr) ||
-      (peers->north_a == nullptr) != (peers->north_control == nullptr) ||
-      (peers->south_a == nullptr) != (peers->south_b == nullptr) ||
-      (peers->south_a == nullptr) != (peers->south_control == nullptr)) {
-    return fail(SK_EINVAL, "incomplete peer mapping");
-  }
-  if (peers->north_a && peers->north_rows < std::max(m, 1)) return fail(SK_EINVAL, "bad north_rows");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool has_n = peers->north_a != nullptr, has_s = peers->south_a != nullptr;
-  const size_t es = dtype_size(d.dtype);
-  const long long row_bytes = pitch * static_cast<long long>(es);
-  long long* ctl = static_cast<long long*>(d_control);
-  const long long* flag_n = has_n ? ctl + 0 : nullptr;  // north halo arrivals (from p-1)
-  const long long* flag_s = has_s ? ctl + 1 : nullptr;  // south halo arrivals (from p+1)
-  unsigned* done = reinterpret_cast<unsigned*>(ctl + 2);
-  // I deliver the north neighbour's SOUTH halo (its flag 1) and the south
-  // neighbour's NORTH halo (its flag 0).
-  long long* pflag_n = has_n ? static_cast<long long*>(peers->north_control) + 1 : nullptr;
-  long long* pflag_s = has_s ? static_cast<long long*>(peers->south_control) + 0 : nullptr;
-  DeviceInfo info;
-  if (int rc = current_device_info(&info)) return rc;
-
-  HaloGeom g{};
-  g.pitch = pitch;
-  g.W = static_cast<int>(width);
-  g.h = static_cast<int>(rows);
-  g.above = has_n ? N : 0;
-  g.below = has_s ? S : 0;
-  g.m = m;
-  g.north_rows = S;
-  g.south_rows = N;
-  g.north_off = has_n ? (N + peers->north_rows) * pitch : 0;
-  g.south_off = 0;
-  g.mode = d.border_mode;
-  const long long B = *epoch;
-
-  // Resolve every kernel of the schedule before the first launch.  With CUDA
-  // lazy loading, loading a module may wait for the context's running
-  // kernels; a strip pass spinning on a peer whose launches this thread has
-  // not issued yet (ranks sharing one process) would then never finish.
-  {
-    int dev = 0;
-    if (int rc = current_device_info(&info, &dev)) return rc;
-    KernelAttr ka;
-    if (int rc = kernel_attr(dev, halo_kernel(d), info, &ka)) return rc;
-    if (int rc = kernel_attr(dev, halo_put_kernel(d.dtype), info, &ka)) return rc;
-    if (rows - 2LL * m > 0) {
-      Plan plan;
-      const char* a0 = static_cast<const char*>(d_a) + (N + m) * row_bytes;
-      if (int rc = make_plan(d, width, rows - 2LL * m, pitch, pitch, N, S, wc, wr, a0, &plan)) return rc;
-    }
-  }
-
-  // Fused path: one launch per generation of the one-pass TMA kernel with
-  // the exchange folded into its boundary tile-rows (k_stencil_tma<..., PEER>),
-  // when the TMA plan applies and every mirrored row lies in the first / last
-  // tile-row.  Otherwise the strips + interior schedule below.
-  // Opt-in (SK_PEER_SCHEDULE=fused).  Measured on one B200, one rank, GoL
-  // 8192^2 at 128x8: the PEER instantiation executes 8.9 % more instructions
-  // (the boundary-row remap and checks on every tile) and runs 104.5 us per
-  // generation against 91.5 us for the plain one-pass kernel, worse than the
-  // strips schedule (+7 %).  It is also persistent: its boundary blocks hold
-  // their SMs while they wait for a neighbour's flag, so ranks sharing a GPU
-  // can starve each other - never chosen for peers on this device.
-  Plan fplan;
-  KernelPtr peer_k = nullptr;
-  const char* sched = std::getenv("SK_PEER_SCHEDULE");
-  const bool shared_gpu = (has_n && peer_on_device(peers->north_a)) || (has_s && peer_on_device(peers->south_a));
-  const bool forced = sched && std::strcmp(sched, "fused") == 0;
-  if (forced && (!shared_gpu || std::getenv("SK_PEER_ALLOW_SHARED"))) {
-    int dev = 0;
-    current_device_info(&info, &dev);
-    const char* a0 = static_cast<const char*>(d_a) + N * row_bytes;
-    if (m > 0 && make_plan(d, width, rows, pitch, pitch, g.above, g.below, wc, wr, a0, &fplan) == SK_OK &&
-        fplan.tma && !fplan.driver_handle && fplan.g.tile_rows >= m) {
-      KernelPtr k = peer_tma_kernel(d, fplan.g.K);
-      KernelAttr ka;
-      if (k && kernel_attr(dev, k, info, &ka) == SK_OK && fplan.threads <= ka.max_threads &&
-          fplan.smem <= ka.max_dyn_smem && occupancy(dev, k, fplan.threads, fplan.smem) >= 1) {
-        peer_k = k;
-      }
-    }
-    g_last_error.clear();
-  }
-
-  // generation 0 halos: put the initial boundary rows, publish B + 1
-  {
-    g.wait_value = B;
-    g.signal_value = B + 1;
-    const void* src = static_cast<const char*>(d_a) + N * row_bytes;
-    void* pn = peers->north_a;
-    void* ps = peers->south_a;
-    const long long cells = static_cast<long long>(S + N) * width;
-    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((cells + 255) / 256, 4LL * info.sms)));
-    void* args[] = {const_cast<void**>(&src), &pn, &ps, const_cast<long long**>(&flag_n),
-                    const_cast<long long**>(&flag_s), &pflag_n, &pflag_s, &done, &g};
-    if (int rc = launch_checked(halo_put_kernel(d.dtype), dim3(grid), dim3(256), args, 0, st)) return rc;
-  }
-  const int strip_grid = static_cast<int>(
-      std::max<long long>(1, std::min<long long>((static_cast<long long>(m) * width + 255) / 256, 2LL * info.sms)));
-  if (peer_k) {
-    Plan pl = fplan;
-    pl.kernel = peer_k;
-    PeerTile& pt = pl.g.peer;
-    pt.flag_n = flag_n;
-    pt.flag_s = flag_s;
-    pt.north_off = g.north_off;
-    pt.south_off = 0;
-    pt.north_rows = S;
-    pt.south_rows = N;
-    pt.pflag_n = pflag_n;
-    pt.pflag_s = pflag_s;
-    pt.done = done;
-    pt.boundary_tiles = pl.g.tiles_x * (pl.g.tiles_y >= 2 ? 2 : 1);
-    const long long total_rows = rows + pl.g.above + pl.g.below;
-    void* src = d_a;
-    void* dst = d_b;
-    for (int gen = 1; gen <= iterations; ++gen) {
-      pt.wait_value = B + gen;
-      pt.signal_value = B + gen + 1;
-      pt.peer_n = has_n ? (gen & 1 ? peers->north_b : peers->north_a) : nullptr;
-      pt.peer_s = has_s ? (gen & 1 ? peers->south_b : peers->south_a) : nullptr;
-      const void* s0 = static_cast<const char*>(src) + N * row_bytes;
-      void* d0 = static_cast<char*>(dst) + N * row_bytes;
-      int rc;
-      switch (d.dtype) {
-        case SK_INT32: rc = launch_typed<int32_t>(d, pl, s0, d0, pl.g.above, total_rows, st); break;
-        case SK_FLOAT32: rc = launch_typed<float>(d, pl, s0, d0, pl.g.above, total_rows, st); break;
-        default: rc = launch_typed<double>(d, pl, s0, d0, pl.g.above, total_rows, st);
-      }
-      if (rc) return rc;
-      std::swap(src, dst);
-    }
-    *epoch = B + iterations + 1;
-    if (result_in_b) *result_in_b = iterations % 2;
-    return SK_OK;
-  }
-
-  // Per generation the strips (caller's stream) and the interior (side
-  // stream) run concurrently; a fork/join event pair orders generation g+1
-  // after both halves of generation g (each half reads the other's rows).
-  const long long inner = rows - 2LL * m;
-  SideLane* lane = nullptr;
-  if (inner > 0 && m > 0) {
-    if (int rc = side_lane(st, &lane)) return rc;
-  }
-  void* src = d_a;
-  void* dst = d_b;
-  for (int gen = 1; gen <= iterations; ++gen) {
-    g.wait_value = B + gen;
-    g.signal_value = B + gen + 1;
-    void* pn = has_n ? (gen & 1 ? peers->north_b : peers->north_a) : nullptr;
-    void* ps = has_s ? (gen & 1 ? peers->south_b : peers->south_a) : nullptr;
-    const void* s0 = static_cast<const char*>(src) + N * row_bytes;
-    void* d0 = static_cast<char*>(dst) + N * row_bytes;
-    cudaStream_t ist = st;
-    if (lane) {
-      cudaEventRecord(lane->fork, st);
-      cudaStreamWaitEvent(lane->side, lane->fork, 0);
-      ist = lane->side;
-    }
-    if (m > 0) {
-      int rc;
-      switch (d.dtype) {
-        case SK_INT32:
-          rc = launch_halo_strips<int32_t>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
-          break;
-        case SK_FLOAT32:
-          rc = launch_halo_strips<float>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
-          break;
-        default:
-          rc = launch_halo_strips<double>(d, s0, d0, pn, ps, flag_n, flag_s, pflag_n, pflag_s, done, g, strip_grid, st);
-      }
-      if (rc) return rc;
-    }
-    // interior rows [m, rows - m) read only owned rows (m >= N, S)
-    if (inner > 0) {
-      if (int rc = launch(d, static_cast<const char*>(s0) + m * row_bytes, static_cast<char*>(d0) + m * row_bytes,
-                          width, inner, pitch, pitch, N, S, wc, wr, ist)) {
-        return rc;
-      }
-    }
-    if (lane) {
-      cudaEventRecord(lane->join, lane->side);
-      cudaStreamWaitEvent(st, lane->join, 0);
-    }
-    std::swap(src, dst);
-  }
-  *epoch = B + iterations + 1;
-  if (result_in_b) *result_in_b = iterations % 2;
   return SK_OK;
 }
 

@@ -170,6 +170,31 @@ __device__ __forceinline__ T acc_div(typename Acc<T>::type s, int count) {
   else return s / T(count);
 }
 
+// fp32 s / D, correctly rounded, for a compile-time divisor: q0 = s * RN(1/D),
+// the exact remainder r = s - q0 D (one FMA), q = q0 + r * RN(1/D).  Away
+// from zero, subnormals, overflow and non-finite s this equals the IEEE
+// quotient for D = 28 - verified for all 2^32 inputs on the GPU
+// (tests/test_div_const.py) - and costs 3 FP instructions instead of the
+// ~11 of a general division (MUFU.RCP, 4 FFMA, FCHK and its slow-path
+// branch).  The rare out-of-range inputs take the IEEE division.
+template <int D>
+__device__ __forceinline__ float div_const_rn(float s) {
+  constexpr float y = 1.0f / static_cast<float>(D);
+  const float q0 = __fmul_rn(s, y);
+  const float r = __fmaf_rn(-q0, static_cast<float>(D), s);
+  const float q = __fmaf_rn(r, y, q0);
+  const float a = fabsf(s);
+  return (a >= 0x1p-100f && a <= 0x1p+120f) ? q : __fdiv_rn(s, static_cast<float>(D));
+}
+
+// Division by a compile-time cell count: the exact fp32 sequence above for
+// the divisors it is verified for, the IEEE division otherwise.
+template <typename T, int D>
+__device__ __forceinline__ T acc_div_const(typename Acc<T>::type s) {
+  if constexpr (std::is_same_v<T, float> && D == 28) return div_const_rn<D>(s);
+  else return acc_div<T>(s, D);
+}
+
 struct BoxMean {
   template <typename T, class V>
   __device__ __forceinline__ T apply(const V& v, const OpParams<T>& p) const {
@@ -210,7 +235,7 @@ struct BoxMeanFixed {
       for (int dc = -W + 1; dc <= E; ++dc) row = acc_add<T>(row, v.at(dr, dc));
       s = dr == -N ? row : acc_add2<T>(s, row);
     }
-    return acc_div<T>(s, kCount);
+    return acc_div_const<T, kCount>(s);
   }
 
   template <typename T, int K>
@@ -225,7 +250,7 @@ struct BoxMeanFixed {
       A s = rows[k];
 #pragma unroll
       for (int j = 1; j <= N + S; ++j) s = acc_add2<T>(s, rows[k + j]);
-      res[k] = acc_div<T>(s, kCount);
+      res[k] = acc_div_const<T, kCount>(s);
     }
   }
 };
