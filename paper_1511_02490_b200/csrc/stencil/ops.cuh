@@ -178,13 +178,19 @@ __device__ __forceinline__ T acc_div(typename Acc<T>::type s, int count) {
 // ~11 of a general division (MUFU.RCP, 4 FFMA, FCHK and its slow-path
 // branch).  The rare out-of-range inputs take the IEEE division.
 template <int D>
-__device__ __forceinline__ float div_const_rn(float s) {
+__device__ __forceinline__ float div_const_fast(float s) {
   constexpr float y = 1.0f / static_cast<float>(D);
   const float q0 = __fmul_rn(s, y);
   const float r = __fmaf_rn(-q0, static_cast<float>(D), s);
-  const float q = __fmaf_rn(r, y, q0);
+  return __fmaf_rn(r, y, q0);
+}
+__device__ __forceinline__ bool div_const_in_range(float s) {
   const float a = fabsf(s);
-  return (a >= 0x1p-100f && a <= 0x1p+120f) ? q : __fdiv_rn(s, static_cast<float>(D));
+  return a >= 0x1p-100f && a <= 0x1p+120f;  // false for 0, subnormals, inf, NaN
+}
+template <int D>
+__device__ __forceinline__ float div_const_rn(float s) {
+  return div_const_in_range(s) ? div_const_fast<D>(s) : __fdiv_rn(s, static_cast<float>(D));
 }
 
 // Division by a compile-time cell count: the exact fp32 sequence above for
@@ -245,12 +251,30 @@ struct BoxMeanFixed {
     A rows[K + N + S];
 #pragma unroll
     for (int i = 0; i < K + N + S; ++i) rows[i] = row_sum<T>(centre + (i - N) * pitch);
+    A sums[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       A s = rows[k];
 #pragma unroll
       for (int j = 1; j <= N + S; ++j) s = acc_add2<T>(s, rows[k + j]);
-      res[k] = acc_div_const<T, kCount>(s);
+      sums[k] = s;
+    }
+    if constexpr (std::is_same_v<T, float> && kCount == 28) {
+      // one branch per work-item: the K quotients take the 3-instruction
+      // exact sequence unless one of them is out of its range
+      bool fast = true;
+#pragma unroll
+      for (int k = 0; k < K; ++k) fast = fast && div_const_in_range(sums[k]);
+      if (fast) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) res[k] = div_const_fast<kCount>(sums[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) res[k] = __fdiv_rn(sums[k], static_cast<float>(kCount));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) res[k] = acc_div_const<T, kCount>(sums[k]);
     }
   }
 };

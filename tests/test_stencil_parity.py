@@ -369,3 +369,29 @@ def test_streamed_host_jobs_match_run_host():
         assert want.tobytes() == O.iterate(O.desc_from_stencil(st), x, it).tobytes()
     with pytest.raises(Exception):
         st.wait_host(10 ** 9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["auto", "explicit"])
+def test_boxmean_division_special_values(path):
+    """Config-4 boxmean divides by 28 with the exact 3-instruction sequence
+    (ops.cuh div_const_fast) and falls back to IEEE division for a
+    work-item whose sums include zeros, subnormals, huge values or inf:
+    both branches must equal the oracle's s / 28 bit for bit."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    x = (rng.random((200, 300)) - 0.5).astype(np.float32)
+    x[10:20, :] = 0.0
+    x[30:40, :] = (rng.random((10, 300)) * 1e-40).astype(np.float32)   # subnormal sums
+    x[50:52, 100:120] = np.float32(3e37)                               # beyond the fast range
+    x[60, 7] = np.inf
+    x[80:82, :] = -0.0
+    st = Stencil(op="boxmean", dtype="float32", north=5, south=1, east=3, west=0,
+                 border="nearest", load_path=path)
+    a = torch.from_numpy(x).cuda()
+    b = torch.empty_like(a)
+    st(a, b, 64, 4)
+    torch.cuda.synchronize()
+    want = O.stencil(O.desc_from_stencil(st), x)
+    assert b.cpu().numpy().tobytes() == want.tobytes()
