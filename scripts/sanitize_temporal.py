@@ -24,7 +24,7 @@ elif kind == "bitplane":
     st.iterate(x, torch.empty_like(x), 15, 32, 4)
 elif kind == "fused":
     st = Stencil(op="heat", dtype="float32", border="nearest", load_path="tma", fused_iterations=4)
-    x = torch.from_numpy(rng.random((70, 130)).astype(np.float32)).cuda()
+    x = torch.from_numpy(rng.random((70, 128)).astype(np.float32)).cuda()
     st.iterate(x, torch.empty_like(x), 9, 32, 4)
 elif kind == "peer":
     from paper_1511_02490_b200.distributed import RowShard, iterate_sharded_peer, local_links, new_control
