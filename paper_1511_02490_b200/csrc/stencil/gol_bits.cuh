@@ -169,7 +169,7 @@ __device__ __forceinline__ void strips_substitute(uint32_t (&w)[R], const StripG
 // Register budget per thread bounds the block: R words of state plus the
 // rolling window (the per-kernel maximum workgroup size).
 template <int R>
-__global__ void __launch_bounds__(R <= 8 ? 768 : (R <= 16 ? 384 : 256), R == 16 ? 3 : 1)
+__global__ void __launch_bounds__(R <= 8 ? 768 : (R <= 16 ? 512 : 256))
     k_gol_strips(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, const StripGeom g) {
   extern __shared__ __align__(16) uint32_t sm_x[];
   const int lane = threadIdx.x & 31;
