@@ -26,6 +26,7 @@
 
 #include "wgtb/evaluation.hpp"
 #include "wgtb/executor.hpp"
+#include "wgtb/kernelgen.hpp"
 #include "wgtb/io.hpp"
 #include "wgtb/learn.hpp"
 
@@ -333,11 +334,24 @@ int cmd_features(const Args& a) {
   return 0;
 }
 
+// Executable synthetic kernel for a descriptor (§8f rank 3): writes
+// <out>/<name>.cu (the CUDA functor + sk_gen_table) and <out>/<name>_ref.c.
+int cmd_gen_kernel(const Args& a) {
+  const KernelDescriptor k = kernel_from_json(nlohmann::json::parse(read_text(a.need("--kernel-json"))));
+  const GeneratedKernel g = generate_kernel(k);
+  const fs::path out = a.need("--out");
+  fs::create_directories(out);
+  write_text(out / (k.name + ".cu"), g.cuda);
+  write_text(out / (k.name + "_ref.c"), g.c_ref);
+  std::cout << "generated " << g.functor << " -> " << (out / (k.name + ".cu")).string() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: wgtb generate|collect|evaluate|train|predict|features [options]\n";
+    std::cerr << "usage: wgtb generate|collect|evaluate|train|predict|features|gen-kernel [options]\n";
     return 2;
   }
   const std::string cmd = argv[1];
@@ -350,6 +364,7 @@ int main(int argc, char** argv) {
     if (cmd == "train") return cmd_train(a);
     if (cmd == "predict") return cmd_predict(a);
     if (cmd == "features") return cmd_features(a);
+    if (cmd == "gen-kernel") return cmd_gen_kernel(a);
     throw UsageError("unknown subcommand '" + cmd + "'");
   } catch (const UsageError& e) {
     std::cerr << "wgtb: " << e.what() << "\n";
