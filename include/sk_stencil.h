@@ -197,7 +197,9 @@ int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_o
  * j-1's D2H run on the copy engines while job j computes.  A submit waits
  * only for the job three tickets back (its slot's buffers).  sk_stencil_wait_host
  * blocks until job `ticket` has landed in its h_out.  Same results as
- * sk_stencil_run_host, which is the one-job-at-a-time form. */
+ * sk_stencil_run_host, which is the one-job-at-a-time form (both replace the
+ * SkelCL user call on host data; the reference only
+ * simulates it, simoracle.hpp:45). */
 int sk_stencil_submit_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,
                            int64_t width, int64_t height, int32_t iterations, int32_t wc,
                            int32_t wr, int64_t* ticket);
@@ -259,7 +261,9 @@ typedef struct {
 } sk_ipc_handle;
 
 /* Export / import a device pointer across processes (cudaIpc*MemHandle;
- * peer access is enabled lazily on import). */
+ * peer access is enabled lazily on import).  No reference counterpart: the
+ * reference is single-device; the row-shard exchange is the north star's
+ * addition. */
 int sk_ipc_export(const void* d_ptr, sk_ipc_handle* out);
 int sk_ipc_import(const sk_ipc_handle* h, void** d_ptr);
 int sk_ipc_close(void* d_ptr);
