@@ -277,56 +277,37 @@ __global__ void __launch_bounds__(256)
 
 // packed rows [0, rows) -> T rows: lane = 4 cells (one int4/float4 store),
 // 8 lanes per word, a warp writes 4 words = 128 cells per store instruction.
-// Each warp handles kUnpackBatch items per trip with all their word loads
-// issued first: one dependent load -> store per trip left the kernel
-// latency-bound (4.3 TB/s of writes, ncu).
-constexpr int kUnpackBatch = 4;
-
-template <typename T>
-__device__ __forceinline__ void unpack_store(uint32_t bits, T* o, int col, int W, int vec_store) {
-  using V = typename Vec4<T>::type;
-  if (vec_store && col + 3 < W) {
-    V v;
-    v.x = T(bits & 1u);
-    v.y = T((bits >> 1) & 1u);
-    v.z = T((bits >> 2) & 1u);
-    v.w = T((bits >> 3) & 1u);
-    *reinterpret_cast<V*>(o) = v;
-  } else {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (col + b < W) o[b] = T((bits >> b) & 1u);
-    }
-  }
-}
-
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_gol_unpack(const uint32_t* __restrict__ in, long long pw, int rows, int W,
                  T* __restrict__ out, long long pitch_out, int vec_store) {
+  using V = typename Vec4<T>::type;
   const int lane = threadIdx.x & 31;
   const int nwords = (W + 31) / 32;
   const int groups = (nwords + 3) / 4;  // 4-word groups per row
   const int nib = (lane & 7) * 4;
-  const long long total = static_cast<long long>(rows) * groups;
-  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  for (long long base = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       base < total; base += kUnpackBatch * stride) {
-    uint32_t bits[kUnpackBatch];
-    int r[kUnpackBatch], wd[kUnpackBatch];
+  const long long nwarp_total = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       item < static_cast<long long>(rows) * groups; item += nwarp_total) {
+    const int r = static_cast<int>(item / groups);
+    const int gq = static_cast<int>(item - static_cast<long long>(r) * groups);
+    const int wd = 4 * gq + (lane >> 3);
+    if (wd >= nwords) continue;
+    const uint32_t bits = in[static_cast<long long>(r) * pw + wd] >> nib;
+    const int col = 32 * wd + nib;
+    T* o = out + static_cast<long long>(r) * pitch_out + col;
+    if (vec_store && col + 3 < W) {
+      V v;
+      v.x = T(bits & 1u);
+      v.y = T((bits >> 1) & 1u);
+      v.z = T((bits >> 2) & 1u);
+      v.w = T((bits >> 3) & 1u);
+      *reinterpret_cast<V*>(o) = v;
+    } else {
 #pragma unroll
-    for (int u = 0; u < kUnpackBatch; ++u) {
-      const long long item = base + u * stride;
-      r[u] = static_cast<int>(item / groups);
-      wd[u] = 4 * static_cast<int>(item - static_cast<long long>(r[u]) * groups) + (lane >> 3);
-      bits[u] = (item < total && wd[u] < nwords) ? in[static_cast<long long>(r[u]) * pw + wd[u]] >> nib : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < kUnpackBatch; ++u) {
-      const long long item = base + u * stride;
-      if (item >= total || wd[u] >= nwords) continue;
-      const int col = 32 * wd[u] + nib;
-      unpack_store<T>(bits[u], out + static_cast<long long>(r[u]) * pitch_out + col, col, W, vec_store);
+      for (int b = 0; b < 4; ++b) {
+        if (col + b < W) o[b] = T((bits >> b) & 1u);
+      }
     }
   }
 }
