@@ -289,7 +289,10 @@ typedef struct {
  * peers' *_a / *_b must be the neighbours' buffers in the roles d_a / d_b
  * play in this call (ranks ping-pong in lockstep: swap them together).
  * Replaces: the per-iteration exchange of the NCCL schedule
- * (paper_1511_02490_b200/distributed.py) - the reference has none (§8e). */
+ * (paper_1511_02490_b200/distributed.py) - the reference has none (§8e).
+ * Environment: SK_PEER_SCHEDULE=fused selects the opt-in one-pass kernel
+ * with the exchange in its boundary tile-rows (refused for
+ * peers on this device unless SK_PEER_ALLOW_SHARED is set - test use). */
 int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
                             int64_t rows, int64_t pitch, int32_t iterations, int32_t wc,
                             int32_t wr, const sk_halo_peers* peers, void* d_control,
