@@ -120,3 +120,34 @@ def test_degenerate_calls_are_einval():
     # zero iterations leave the input untouched and report it in a
     assert lib.sk_stencil_iterate(ctypes.byref(stc.desc), a.data_ptr(), a.data_ptr(), 8, 8, 8, 0, 8, 8,
                                   None, ctypes.byref(in_b)) == N.SK_OK and in_b.value == 0
+
+
+@settings(max_examples=60, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
+@given(op=st.sampled_from(["heat", "five_point", "gol", "boxmean", "sobel"]),
+       dtype=st.sampled_from(["int32", "float32", "float64"]), world=st.integers(2, 4),
+       rows_per_rank=st.integers(12, 40), width=st.integers(1, 200), nearest=st.booleans(),
+       iters=st.integers(1, 9), calls=st.integers(1, 3), tb=st.sampled_from([0, 3, 6]),
+       seed=st.integers(0, 10 ** 6))
+def test_fuzz_peer_schedules(op, dtype, world, rows_per_rank, width, nearest, iters, calls, tb, seed):
+    """Row shards on single-process ranks (one stream each) through
+    sk_stencil_iterate_peer: one-generation schedule for every op, and the
+    temporally blocked schedule (TB-deep halos) for heat / five_point."""
+    from test_peer_halo import run_ranks
+
+    n = s = e = w = 1
+    if op == "boxmean":
+        n, s, e, w = 5, 1, 3, 0
+    fused = tb if op in ("heat", "five_point") else 0
+    kw = {"load_path": "strips", "fused_iterations": fused} if fused else {}
+    stc = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w,
+                  border="nearest" if nearest else "pad", pad_value=0.5, **kw)
+    x = make_grid(op, dtype, (world * rows_per_rank, width), seed)
+    try:
+        got = run_ranks(stc, x, world, iters, wc=32, wr=4, calls=min(calls, iters))
+    except (RefusedParameter, IllegalWorkgroupSize):
+        return
+    except N.NativeError as exc:  # a shard too thin for TB-deep strips
+        assert exc.code == N.SK_EINVAL and fused, str(exc)
+        return
+    want = O.iterate(O.desc_from_stencil(stc), x, iters)
+    assert got.tobytes() == want.tobytes(), repr(stc)
