@@ -187,7 +187,8 @@ def run_ours(args):
                  pad_value=pad)
     tdt = {"int32": torch.int32, "float32": torch.float32}[dtype]
     es = 4
-    H = H1 * world  # weak scaling: H1 rows per rank
+    # weak scaling: H1 rows per rank; strong: the H1-row grid split across ranks
+    H = H1 * world if args.scaling == "weak" else H1
     shard = RowShard(H, W, rank, world, n, s)
 
     # deterministic input: the reference Rng stream (kind 2: alive w.p. 0.5)
@@ -323,12 +324,12 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": dtype,
             "data": "synthetic (reference Rng stream, seeded)",
             "config": {
-                "workload": f"{args.config} {W}x{H1} per GPU, {dtype}, {border} {pad}, "
+                "workload": f"{args.config} {W}x{shard.rows} per GPU, {dtype}, {border} {pad}, "
                             f"{iters} iterations/step (BASELINE.json configs[1])",
                 "global_grid": f"{W}x{H}",
                 "iterations_per_step": iters,
@@ -661,6 +662,8 @@ def main():
                     help="skip the temporally blocked leg (TB generations per launch)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange halos between passes instead of behind the interior")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = the configured grid per rank; strong = that grid split across ranks")
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="N>1 halo exchange: peer stores from the strip kernel (CUDA IPC over "
                          "NVLink) or NCCL send/recv behind the interior")

@@ -51,3 +51,14 @@ def test_bench_two_ranks_heat_temporal_leg():
     assert d["config"]["transport"] == "peer"
     t = d["temporal_blocking"]
     assert t and t["bit_exact_vs_one_pass"] and t["value"] > 0
+
+
+def test_bench_two_ranks_strong_scaling():
+    """--scaling strong splits the configured grid across the ranks."""
+    proc = torchrun(2, "bench.py", "--gpus", "2", "--scaling", "strong", "--steps", "1", "--warmup", "3",
+                    "--wc", "32", "--wr", "8", "--no-cpu", "--no-e2e", "--backend", "gloo")
+    lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
+    assert proc.returncode == 0 and len(lines) == 1, proc.stdout + proc.stderr[-3000:]
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["config"]["global_grid"] == "8192x8192"
+    assert "8192x4096 per GPU" in d["config"]["workload"]
