@@ -25,4 +25,10 @@ for k in strips bitplane fused peer streamed; do
   timeout 300 compute-sanitizer --tool memcheck python scripts/sanitize_temporal.py $k >> $O/sanitizer_memcheck.log 2>&1
 done
 grep -E "ERROR SUMMARY|RACECHECK SUMMARY" $O/sanitizer_*.log | sort | uniq -c
+# digests + raw pages stay; the .ncu-rep files would exceed gpurun's 64 MiB copy-back
+for p in prof_gol_128x8 prof_strips_heat prof_bits; do
+  python scripts/ncu_digest.py $O/$p.ncu-rep > $O/${p}_digest.txt 2>/dev/null
+  ncu -i $O/$p.ncu-rep --page raw --csv > $O/${p}_raw.csv 2>/dev/null
+  [ -s $O/${p}_digest.txt ] && rm -f $O/$p.ncu-rep
+done
 ls -la $O
