@@ -36,6 +36,8 @@ def tree(dst: Path, sass: bool):
     src_sass = B200 / "descriptors_sass" / "kernels"
     for p in sorted((B200 / "descriptors" / "kernels").glob("*.json")):
         k = json.loads(p.read_text())
+        if k["name"].startswith("synthetic-") and not (GEN / "lib" / f"lib{k['name']}.so").exists():
+            continue  # only kernels that were generated (and swept) take part
         if sass:
             if k["name"].startswith("synthetic-"):
                 funcs = sf.sass_functions(GEN / "lib" / f"lib{k['name']}.so")
