@@ -19,3 +19,6 @@ timeout "${SWEEP_SECONDS:-3000}" $BIN collect --scenarios results/b200/descripto
   2> "$OUT/collect.log" || echo "collect stopped (rc=$?)"
 tail -3 "$OUT/collect.log"
 wc -l "$OUT/contexts.csv"
+# gpurun copies back at most 64 MiB: ship the samples compressed
+gzip -f "$OUT/samples.csv"
+rm -rf "$OUT/descriptors"
