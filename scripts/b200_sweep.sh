@@ -1,7 +1,8 @@
 #!/usr/bin/env bash
 # Exhaustive wc x wr sweep on the B200 for the autotuning study (BASELINE
-# config 5): 24 synthetic kernels (seed 17) + the 6 reference kernels x the
-# 12 standard datasets.  Resumable: completed scenarios in results/b200 are
+# config 5): the 40 synthetic kernels of generate_kernels(40, 17) + the 6
+# reference kernels x the descriptor datasets (results/b200/descriptors; pass
+# --dataset / --kernel filters through to `wgtb collect`).  Resumable: completed scenarios in results/b200 are
 # kept.  Output lands in gpurun_out/b200 (copy back into results/b200).
 set -euo pipefail
 cd "$(dirname "$0")/.."
