@@ -33,6 +33,31 @@ CONFIGS = {
     "gol": ("gol", "int32", 8192, 8192, 100, "pad", 0.0, (1, 1, 1, 1)),
     "heat": ("heat", "float32", 16384, 16384, 100, "nearest", 0.0, (1, 1, 1, 1)),
 }
+# input stream per config: (fill kind, seed); rank p of a
+# weak-scaling run uses seed + p for its own block of rows
+INPUTS = {"gol": (2, 2), "heat": (1, 3)}
+# generations compared bit-exactly against the CPU baseline (config 3's
+# parity is stated at 10 generations)
+PARITY_GENERATIONS = {"gol": 100, "heat": 10}
+BASELINE_LABEL = {"gol": "BASELINE.json configs[1]", "heat": "BASELINE.json configs[2]"}
+
+
+def workload_config(config: str, world: int, scaling: str) -> dict:
+    """The `config` object, identical in both arms (ours / --impl reference)."""
+    op, dtype, H1, W, iters, border, pad, _ = CONFIGS[config]
+    H = H1 * world if scaling == "weak" else H1
+    rows = H // world
+    es = np.dtype(dtype).itemsize
+    per = "per GPU" if scaling == "weak" else "global"
+    return {
+        "workload": f"{config} {W}x{H1} {per}, {dtype}, {border} {pad}, {iters} generations/step "
+                    f"({BASELINE_LABEL[config]})",
+        "global_grid": f"{W}x{H}",
+        "iterations_per_step": iters,
+        "input": "reference Rng stream (mt19937_64) kind %d seed %d" % INPUTS[config],
+        "l2": f"inputs larger than L2 ({rows * W * es / 1e6:.0f} MB per buffer per GPU)",
+        "parallelism": f"row-shard x{world} ({scaling} scaling)",
+    }
 
 
 KERNEL_NAMES = {"gol": "k_stencil_tma<Gol,int>", "heat": "k_stencil_tma<Heat,float>"}
@@ -128,12 +153,14 @@ def traffic_for(config: str, block: str):
 
 
 # --------------------------------------------------------------------- ours
-def predict_block(st, config: str, W: int, H: int):
+def predict_block(st, config: str, W: int, H: int, held_out: bool = False):
     """The autotuner's prediction (in-process wgtb_predict: the trained bundle
-    + live device probes) for this scenario, or None without a bundle."""
+    + live device probes) for this scenario, or None without a bundle.
+    held_out: the bundle trained without any scenario of this kernel."""
     from paper_1511_02490_b200 import autotune
 
-    model = ROOT / "results" / "b200" / "model.json"
+    kname = "he" if config == "heat" else config
+    model = ROOT / "results" / "b200" / (f"model_loko_{kname}.json" if held_out else "model.json")
     kernel = ROOT / "results" / "b200" / "descriptors" / "kernels" / f"{'he' if config == 'heat' else config}.json"
     if not (model.exists() and kernel.exists()):
         return None, "no trained model bundle (results/b200/model.json)"
@@ -142,10 +169,11 @@ def predict_block(st, config: str, W: int, H: int):
     return (r["wc"], r["wr"]), f"{tech} ({r['probes']} live probe(s), {r['ms']:.3f} ms)"
 
 
-def quick_sweep(st, a, b, W, H):
+def quick_sweep(st, a, b, W, H, top_n=12, fine_samples=8):
     """Exhaustive wc x wr sweep of one pass (the tuner's oracle on this box):
     every even size with area <= 1024 (enumerate_space, space.cpp:134-145),
-    2 samples each, then the best 12 re-timed with 8 samples (L2 flushed)."""
+    2 samples each, then the best `top_n` re-timed with `fine_samples`
+    samples (L2 flushed)."""
     from paper_1511_02490_b200 import IllegalWorkgroupSize, RefusedParameter
 
     sizes = [(c, r) for c in range(2, 513, 2) for r in range(2, 1024 // c + 1, 2)]
@@ -156,11 +184,71 @@ def quick_sweep(st, a, b, W, H):
         except (IllegalWorkgroupSize, RefusedParameter):
             continue
         res[(wc, wr)] = sum(ms) / len(ms)
-    top = sorted(res, key=lambda k: res[k])[:12]
-    fine = {k: float(np.mean(st.time(a, b, k[0], k[1], samples=8, warmup=1, flush_l2=True)))
+    top = sorted(res, key=lambda k: res[k])[:top_n]
+    fine = {k: float(np.mean(st.time(a, b, k[0], k[1], samples=fine_samples, warmup=1,
+                                     flush_l2=True)))
             for k in top}
     best = min(fine, key=lambda k: (fine[k], k))
     return best, fine[best], res
+
+
+def tune_block(st, config, a, b, W, H):
+    """Oracle block on this box + the autotuner's predictions for it."""
+    t0 = time.time()
+    (wc, wr), best_ms, res = quick_sweep(st, a, b, W, H)
+    worst = max(res.values())
+    info = {"sizes_timed": len(res), "oracle_block": f"{wc}x{wr}",
+            "oracle_pass_ms": round(best_ms, 5),
+            "oracle_over_worst": round(worst / best_ms, 2),
+            "sweep_s": round(time.time() - t0, 1)}
+
+    def perf_of(pred):
+        pms = float(np.mean(st.time(a, b, pred[0], pred[1], samples=8, warmup=1, flush_l2=True)))
+        return pms, round(min(1.0, best_ms / pms), 4)
+
+    pred, how = predict_block(st, config, W, H)
+    if pred:
+        pms, p = perf_of(pred)
+        info.update({"predicted_block": f"{pred[0]}x{pred[1]}", "technique": how,
+                     "predicted_pass_ms": round(pms, 5), "predicted_over_oracle": p})
+    else:
+        info["predicted_over_oracle"] = None
+        info["prediction_note"] = how
+    # held out: a bundle trained without this kernel's scenarios
+    # (leave-one-kernel-out), so the prediction is not in-sample
+    pred_h, how_h = predict_block(st, config, W, H, held_out=True)
+    if pred_h:
+        pms, p = perf_of(pred_h)
+        info["held_out"] = {"predicted_block": f"{pred_h[0]}x{pred_h[1]}", "technique": how_h,
+                            "predicted_pass_ms": round(pms, 5), "predicted_over_oracle": p}
+    # the human-expert and common fixed sizes (PAPER.md:748-750, bench.cpp:550-566)
+    for k in ((32, 4), (4, 4), (32, 8)):
+        if k in res:
+            info[f"perf_{k[0]}x{k[1]}"] = round(min(res.values()) / res[k], 4)
+    return info
+
+
+def _seeded_rows(config: str, rows: int, W: int, rank: int, scaling: str, world: int):
+    """This rank's owned rows of the seeded input.  Weak scaling: rank p's
+    block is its own seeded grid (seed + p); strong: rank p's slice of the one
+    global grid (seed)."""
+    op, dtype, H1, _, _, _, _, _ = CONFIGS[config]
+    kind, seed = INPUTS[config]
+    if scaling == "weak" or world == 1:
+        return _fill((rows, W), dtype, kind, seed + rank)
+    full = _fill((H1, W), dtype, kind, seed)
+    r0 = rank * H1 // world
+    return np.ascontiguousarray(full[r0:r0 + rows])
+
+
+def _fill(shape, dtype, kind, seed):
+    """Seeded input through the product library (sk_fill_host); the reference
+    arm makes the identical stream with oracle_fill (tests/test_abi.py)."""
+    from paper_1511_02490_b200 import fill_host
+
+    a = np.empty(shape, dtype=dtype)
+    fill_host(a, kind, seed)
+    return a
 
 
 def run_ours(args):
@@ -174,7 +262,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    local = local % max(1, torch.cuda.device_count())  # --backend gloo may share one GPU
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    ndev = torch.cuda.device_count()
+    if args.backend == "nccl" and world > ndev:
+        raise SystemExit(f"--gpus {world} needs {world} GPUs, this node has {ndev} "
+                         "(--backend gloo shares one GPU for testing)")
+    local = local % max(1, ndev)  # --backend gloo may share one GPU
     torch.cuda.set_device(local)
     if world > 1:
         if args.backend == "nccl":
@@ -186,18 +280,15 @@ def run_ours(args):
     st = Stencil(op=op, dtype=dtype, north=n, south=s, east=e, west=w, border=border,
                  pad_value=pad)
     tdt = {"int32": torch.int32, "float32": torch.float32}[dtype]
-    es = 4
+    es = np.dtype(dtype).itemsize
     # weak scaling: H1 rows per rank; strong: the H1-row grid split across ranks
     H = H1 * world if args.scaling == "weak" else H1
     shard = RowShard(H, W, rank, world, n, s)
-
-    # deterministic input: the reference Rng stream (kind 2: alive w.p. 0.5)
-    from paper_1511_02490_b200 import fill_host
-    host = np.empty((shard.rows, W), dtype=dtype)
-    fill_host(host, 2 if dtype == "int32" else 1, 2 + rank)
+    host = _seeded_rows(args.config, shard.rows, W, rank, args.scaling, world)
     a = torch.zeros((shard.buffer_rows, W), dtype=tdt, device="cuda")
     a[shard.north:shard.north + shard.rows] = torch.from_numpy(host).cuda()
     b = torch.zeros_like(a)
+    x0 = a.clone()
 
     # ---- tuned block size (exhaustive sweep of one pass on this box)
     sweep_info = {}
@@ -205,30 +296,10 @@ def run_ours(args):
         wc, wr = args.wc, args.wr
     else:
         if rank == 0:
-            t0 = time.time()
-            (wc, wr), best_ms, res = quick_sweep(st, a[shard.north:shard.north + shard.rows],
-                                                 b[shard.north:shard.north + shard.rows], W,
-                                                 shard.rows)
-            worst = max(res.values())
-            sweep_info = {"sizes_timed": len(res), "oracle_block": f"{wc}x{wr}",
-                          "oracle_pass_ms": round(best_ms, 5),
-                          "oracle_over_worst": round(worst / best_ms, 2),
-                          "sweep_s": round(time.time() - t0, 1)}
-            pred, how = predict_block(st, args.config, W, shard.rows)
-            if pred:
-                pv = b[shard.north:shard.north + shard.rows]
-                pa = a[shard.north:shard.north + shard.rows]
-                pms = float(np.mean(st.time(pa, pv, pred[0], pred[1], samples=8, warmup=1,
-                                            flush_l2=True)))
-                sweep_info.update({"predicted_block": f"{pred[0]}x{pred[1]}", "technique": how,
-                                   "predicted_pass_ms": round(pms, 5),
-                                   "predicted_over_oracle": round(min(1.0, best_ms / pms), 4)})
-            else:
-                sweep_info["predicted_over_oracle"] = None
-                sweep_info["prediction_note"] = how
-            for k in ((32, 4), (4, 4), (32, 8)):
-                if k in res:
-                    sweep_info[f"perf_{k[0]}x{k[1]}"] = round(min(res.values()) / res[k], 4)
+            sweep_info = tune_block(st, args.config,
+                                    a[shard.north:shard.north + shard.rows],
+                                    b[shard.north:shard.north + shard.rows], W, shard.rows)
+            wc, wr = map(int, sweep_info["oracle_block"].split("x"))
         else:
             wc = wr = 0
         if world > 1:
@@ -286,32 +357,55 @@ def run_ours(args):
                          dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-    launches = args.steps * iters
-    if world > 1:  # boundary strips + interior per generation (+ the initial put: peer)
-        launches = args.steps * (2 * iters + (1 if links is not None else 0))
+    # launches of our kernels in the timed region: one pass per generation at
+    # N=1; at N>1 the peer schedule runs strips + interior per generation
+    # (+ one initial put per call), the NCCL schedule two strips + interior
+    if world == 1:
+        per_gen, per_call = 1, 0
+    elif links is not None:
+        per_gen, per_call = 2, 1
+    else:
+        per_gen, per_call = (3, 0) if not args.no_overlap else (1, 0)
+    launches = args.steps * (per_gen * iters + per_call)
     cells_total = float(H) * W * iters * args.steps
     gcells = cells_total / (ms / 1e3) / 1e9
     peak, peak_kind = measured_hbm_peak()
-    per_launch_s = ms / 1e3 / launches
-    bytes_per_launch = float(shard.rows) * W * 2 * es
-    achieved = bytes_per_launch / per_launch_s / 1e9
+    # algorithmic bytes of one generation of this rank's shard (read + write
+    # of every owned cell), per generation - not per launch, since a
+    # generation is several launches at N>1
+    per_gen_s = ms / 1e3 / (args.steps * iters)
+    bytes_per_gen = float(shard.rows) * W * 2 * es
+    achieved = bytes_per_gen / per_gen_s / 1e9
+
+    # ---- parity at the full workload: the same step from the seeded input
+    # against the CPU baseline (N=1), bit for bit
+    parity = None
+    cpu = None
+    if world == 1:
+        a.copy_(x0)
+        got = one_step()
+        torch.cuda.synchronize()
+        gpu_result = shard.owned(got).cpu().numpy()
+        if not args.no_cpu:
+            cpu, parity = cpu_baseline_and_parity(args.config, host, gpu_result, st, wc, wr,
+                                                  threads=os.cpu_count() or 1)
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         e2e = e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world)
 
-    # ---- temporally blocked path on the same workload (rank 0, N=1 only)
+    # ---- temporally blocked path on the same workload
     temporal = None
     if rank == 0 and world == 1 and not args.no_temporal:
         temporal = temporal_leg(args, host, tdt, wc, wr, iters, peak)
     elif world > 1 and args.config == "heat" and links is not None and not args.no_temporal:
         temporal = temporal_leg_sharded(args, host, shard, wc, wr, iters, world, rank)
 
-    # ---- CPU baseline (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, threads=os.cpu_count() or 1)
+    # ---- the other BASELINE configs (N=1: configs 1, 3, 4; N>1: config 3)
+    others = None
+    if not args.no_configs:
+        others = other_configs(args, world, rank, peak)
 
     if rank == 0:
         traffic = traffic_for(args.config, block)
@@ -328,30 +422,24 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": dtype,
             "data": "synthetic (reference Rng stream, seeded)",
-            "config": {
-                "workload": f"{args.config} {W}x{shard.rows} per GPU, {dtype}, {border} {pad}, "
-                            f"{iters} iterations/step (BASELINE.json configs[1])",
-                "global_grid": f"{W}x{H}",
-                "iterations_per_step": iters,
-                "block": block,
-                "l2": f"inputs larger than L2 ({shard.rows * W * es / 1e6:.0f} MB per buffer)",
-                "parallelism": f"row-shard x{world}" + (
-                    (" + peer-memory halo exchange fused into the strip kernel"
-                     if links is not None else " + NCCL halo exchange") if world > 1 else ""),
-                "transport": "peer" if links is not None else transport,
-            },
+            "config": workload_config(args.config, world, args.scaling),
+            "block": block,
+            "transport": "peer" if links is not None else transport,
             "hbm_frac": round(achieved / peak, 4),
             "predicted_over_oracle": sweep_info.get("predicted_over_oracle"),
+            "parity": parity,
             "tuning": sweep_info,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic,
-                         "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "avg_launch_us": round(per_launch_s * 1e6, 2),
-                         "kernel": KERNEL_NAMES[args.config]},
+                         "algorithmic_bytes_per_launch": bytes_per_gen,
+                         "avg_launch_us": round(per_gen_s * 1e6, 2),
+                         "kernel": KERNEL_NAMES[args.config],
+                         "note": "per rank, per generation (one launch at N=1)"},
             "cpu_baseline": cpu,
             "temporal_blocking": temporal,
+            "configs": others,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -359,6 +447,8 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and not parity["bit_exact"]:
+        raise SystemExit("parity FAILED: GPU result differs from the CPU baseline")
 
 
 def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
@@ -566,85 +656,302 @@ def temporal_leg_sharded(args, host, shard, wc1, wr1, iters, world, rank,
 # --------------------------------------------------------------- CPU side
 def _oracle():
     sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib  # the CPU restatement: baseline / reference arm only
+    import oracle_lib  # the CPU restatement: baseline / parity / reference arm only
 
     return oracle_lib
 
 
-def cpu_baseline(config: str, threads: int, budget_s: float = 12.0):
-    """The oracle port timed on this host's cores over a bounded sample."""
+def cpu_baseline_and_parity(config: str, host, gpu_result, st, wc, wr, threads: int):
+    """The CPU baseline (oracle/stencil_oracle.c's vectorised rows, all host
+    threads) runs the step's full workload from the same seeded input, is
+    timed, and its result is compared bit for bit with the GPU's.  The first
+    generation is also checked against the per-cell oracle restatement, and a
+    short single-thread sample gives the 1-core figure."""
+    import ctypes
+
     O = _oracle()
     op, dtype, H, W, iters, border, pad, (n, s, e, w) = CONFIGS[config]
-    from paper_1511_02490_b200 import fill_host
-
-    grid = np.empty((H, W), dtype=dtype)
-    fill_host(grid, 2 if dtype == "int32" else 1, 2)
     d = O.desc_from(op, dtype, n, s, e, w, border, pad)
-    out = np.empty_like(grid)
-    done = 0
+    gens = PARITY_GENERATIONS[config]
+    a = np.ascontiguousarray(host).copy()
+    b = np.empty_like(a)
+    b.fill(0)  # first touch outside the timed region
     t0 = time.perf_counter()
-    src, dst = grid, out
-    while done < iters and (time.perf_counter() - t0) < budget_s:
-        import ctypes
-        O.lib().oracle_stencil(ctypes.byref(d), src.ctypes.data, dst.ctypes.data, W, H, W, W, 0,
-                               0, threads)
-        src, dst = dst, src
-        done += 1
+    rc = O.lib().oracle_baseline_iterate(ctypes.byref(d), a.ctypes.data, b.ctypes.data, W, H,
+                                         gens, threads)
     dt = time.perf_counter() - t0
-    return {"value": round(float(H) * W * done / dt / 1e9, 4), "unit": "Gcells/s",
-            "cores": threads, "kind": "port",
-            "sample": f"{done} of {iters} {config} generations on the full {W}x{H} grid "
-                      f"({dt:.1f} s, C oracle, {threads} threads)"}
+    assert rc == 0
+    cpu_res = b if gens % 2 else a
+    # single thread, 2 generations of the same grid
+    a1 = np.ascontiguousarray(host).copy()
+    b1 = np.zeros_like(a1)
+    t1 = time.perf_counter()
+    O.lib().oracle_baseline_iterate(ctypes.byref(d), a1.ctypes.data, b1.ctypes.data, W, H, 2, 1)
+    dt1 = time.perf_counter() - t1
+    # generation 1 against the per-cell restatement (the checker itself)
+    first_ok = bool(O.stencil(d, host, threads=threads).tobytes()
+                    == O.baseline_stencil(d, host, threads=threads).tobytes())
+    if gens == iters:
+        want = cpu_res
+        gpu = gpu_result
+    else:  # parity at `gens` generations (config 3): rerun the GPU to match
+        import torch
+
+        x = torch.from_numpy(np.ascontiguousarray(host)).cuda()
+        gpu = st.iterate(x, torch.empty_like(x), gens, wc, wr).cpu().numpy()
+        want = cpu_res
+    exact = bool(gpu.tobytes() == want.tobytes())
+    nbad = 0 if exact else int(np.count_nonzero(gpu != want))
+    cpu = {"value": round(float(H) * W * gens / dt / 1e9, 4), "unit": "Gcells/s",
+           "cores": threads, "kind": "port",
+           "sample": f"{gens} of {iters} {config} generations on the full {W}x{H} grid "
+                     f"({dt:.2f} s, oracle_baseline_iterate, {threads} threads)",
+           "single_thread": {"value": round(float(H) * W * 2 / dt1 / 1e9, 4), "cores": 1,
+                             "sample": f"2 generations of {W}x{H} ({dt1:.2f} s)"}}
+    parity = {"bit_exact": exact and first_ok, "generations": gens, "grid": f"{W}x{H}",
+              "against": "CPU baseline (oracle_baseline_iterate), whose generation 1 equals "
+                         "the per-cell oracle (oracle_stencil)",
+              "first_generation_baseline_equals_oracle": first_ok, "mismatched_cells": nbad}
+    return cpu, parity
+
+
+def other_configs(args, world, rank, peak):
+    """Lines for the BASELINE configs other than the headline, each with its
+    own parity check against the CPU oracle (N=1), or config 3 sharded (N>1)."""
+    if world > 1:
+        return {"config3_heat": sharded_heat(args, world, rank)}
+    out = {}
+    for fn in (config1_five_point, config3_heat, config4_boxmean):
+        try:
+            out.update(fn(args, peak))
+        except Exception as exc:  # report, never hide
+            out[fn.__name__] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    bad = [k for k, v in out.items() if isinstance(v, dict) and v.get("parity") is False]
+    if bad:
+        print(json.dumps({"parity_failed": bad}), file=sys.stderr)
+        raise SystemExit(f"parity FAILED for {bad}")
+    return out
+
+
+def config1_five_point(args, peak):
+    """Config 1: 5-point, N=S=E=W=1, 1024x1024 f32 (2u-1, seed 1), pad 0 (TMA
+    zero fill) and pad 1 (shared-memory fix-up), one pass.  L2-resident: a
+    parity config, timed only for the record."""
+    import torch
+
+    from paper_1511_02490_b200 import Stencil
+
+    O = _oracle()
+    g = _fill((1024, 1024), "float32", 0, 1)
+    x = torch.from_numpy(g).cuda()
+    y = torch.empty_like(x)
+    res = {}
+    for pad in (0.0, 1.0):
+        st = Stencil(op="five_point", dtype="float32", pad_value=pad)
+        want = O.baseline_stencil(O.desc_from("five_point", "float32", pad=pad), g)
+        exact = True
+        for wc, wr in ((32, 8), (128, 4), (2, 2), (30, 6), (512, 2)):
+            st(x, y, wc, wr)
+            exact &= bool(y.cpu().numpy().tobytes() == want.tobytes())
+        ms = float(np.mean(st.time(x, y, 32, 8, samples=30, warmup=3, flush_l2=True)))
+        res[f"pad{int(pad)}"] = {"parity": exact, "blocks_checked": 5,
+                                 "gcells_s_32x8": round(1024 * 1024 / ms / 1e6, 1)}
+    return {"config1_five_point_1024": res}
+
+
+def config3_heat(args, peak):
+    """Config 3 at one GPU: heat f32 16384^2 nearest, tuned one pass,
+    100 generations per step; parity at 10 generations vs the CPU baseline."""
+    import ctypes
+
+    import torch
+
+    from paper_1511_02490_b200 import Stencil
+
+    O = _oracle()
+    op, dtype, H, W, iters, border, pad, _ = CONFIGS["heat"]
+    st = Stencil(op=op, dtype=dtype, border=border, pad_value=pad)
+    host = _fill((H, W), dtype, *INPUTS["heat"])
+    a = torch.from_numpy(host).cuda()
+    b = torch.empty_like(a)
+    info = tune_block(st, "heat", a, b, W, H)
+    wc, wr = map(int, info["oracle_block"].split("x"))
+    gens = PARITY_GENERATIONS["heat"]
+    got = st.iterate(a.clone(), torch.empty_like(a), gens, wc, wr).cpu().numpy()
+    d = O.desc_from(op, dtype, 1, 1, 1, 1, border, pad)
+    want = O.baseline_iterate(d, host, gens, threads=os.cpu_count() or 1)
+    exact = bool(got.tobytes() == want.tobytes())
+    rel = float(np.max(np.abs(got.astype(np.float64) - want) / np.maximum(np.abs(want), 1e-30)))
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        st.iterate(a, b, iters, wc, wr)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        st.iterate(a, b, iters, wc, wr)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    g = float(H) * W * iters / (ms / 1e3) / 1e9
+    return {"config3_heat_16384": {
+        "value": round(g, 2), "unit": "Gcells/s", "ms_per_step": round(ms, 3),
+        "iterations_per_step": iters, "steps": steps, "block": f"{wc}x{wr}",
+        "hbm_frac": round(g * 8 / peak, 4), "parity": exact, "parity_generations": gens,
+        "max_rel_err": rel, "tolerance": 1e-5, "tuning": info}}
+
+
+def config4_boxmean(args, peak):
+    """Config 4: asymmetric (5,1,3,0) box mean, nearest, 4096^2 f32 (2u-1,
+    seed 4): the full wc x wr sweep (every legal size) and the oracle block's
+    Gcells/s; the oracle block and 50 strided sizes checked vs the CPU oracle."""
+    import torch
+
+    from paper_1511_02490_b200 import IllegalWorkgroupSize, RefusedParameter, Stencil
+
+    O = _oracle()
+    st = Stencil(op="boxmean", dtype="float32", north=5, south=1, east=3, west=0,
+                 border="nearest")
+    host = _fill((4096, 4096), "float32", 0, 4)
+    a = torch.from_numpy(host).cuda()
+    b = torch.empty_like(a)
+    (wc, wr), best_ms, res = quick_sweep(st, a, b, 4096, 4096, top_n=16, fine_samples=30)
+    d = O.desc_from("boxmean", "float32", 5, 1, 3, 0, "nearest")
+    want = O.baseline_stencil(d, host, threads=os.cpu_count() or 1)
+    keys = sorted(res)
+    check = [(wc, wr)] + keys[:: max(1, len(keys) // 50)][:50]
+    bad = []
+    for k in check:
+        try:
+            st(a, b, k[0], k[1])
+        except (IllegalWorkgroupSize, RefusedParameter):
+            continue
+        if b.cpu().numpy().tobytes() != want.tobytes():
+            bad.append(f"{k[0]}x{k[1]}")
+    g = 4096 * 4096 / (best_ms / 1e3) / 1e9
+    return {"config4_boxmean5130_4096": {
+        "oracle_block": f"{wc}x{wr}", "oracle_pass_us": round(best_ms * 1e3, 2),
+        "value": round(g, 1), "unit": "Gcells/s", "hbm_frac": round(g * 8 / peak, 4),
+        "sizes_timed": len(res), "oracle_over_worst": round(max(res.values()) / best_ms, 2),
+        "parity": not bad, "sizes_checked": len(check), "mismatched_sizes": bad[:10],
+        "timing": "2 samples per size, best 16 re-timed with 30 samples, L2 flushed"}}
+
+
+def sharded_heat(args, world, rank):
+    """Config 3 across ranks: heat 16384^2 per GPU (weak) and 16384^2 split
+    (strong), tuned one-pass executor with the halo exchange."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1511_02490_b200 import Stencil
+    from paper_1511_02490_b200.distributed import RowShard, iterate_sharded_overlapped
+
+    op, dtype, H1, W, iters, border, pad, (n, s, e, w) = CONFIGS["heat"]
+    st = Stencil(op=op, dtype=dtype, border=border, pad_value=pad)
+    wc, wr = 104, 6
+    out = {}
+    for scaling in ("weak", "strong"):
+        H = H1 * world if scaling == "weak" else H1
+        shard = RowShard(H, W, rank, world, n, s)
+        host = _seeded_rows("heat", shard.rows, W, rank, scaling, world)
+        a = torch.zeros((shard.buffer_rows, W), dtype=torch.float32, device="cuda")
+        a[n:n + shard.rows] = torch.from_numpy(host).cuda()
+        b = torch.zeros_like(a)
+        gens = 20
+        for _ in range(2):
+            iterate_sharded_overlapped(a, b, shard, gens, st, wc, wr)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            iterate_sharded_overlapped(a, b, shard, gens, st, wc, wr)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 3], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        out[scaling] = {"value": round(float(H) * W * gens / (ms / 1e3) / 1e9, 2),
+                        "unit": "Gcells/s", "grid": f"{W}x{H}", "generations": gens,
+                        "ms": round(ms, 3), "block": f"{wc}x{wr}",
+                        "schedule": "strips + NCCL exchange behind the interior"}
+    return out
 
 
 def run_reference(args):
-    """Reference arm: the CPU implementation of the path on this host's cores."""
+    """Reference arm: the CPU implementation of the path (the oracle port's
+    vectorised baseline; the reference itself has no stencil code, SURVEY.md
+    §0.2) on this host's cores, on the same workload `config` as ours.  It
+    never loads the product library (inputs come from oracle_fill)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     O = _oracle()
     import ctypes
 
-    op, dtype, H, W, iters, border, pad, (n, s, e, w) = CONFIGS[args.config]
-    from paper_1511_02490_b200 import fill_host
-
+    op, dtype, H1, W, iters, border, pad, (n, s, e, w) = CONFIGS[args.config]
+    H = H1 * world if args.scaling == "weak" else H1
     threads = os.cpu_count() or 1
-    grid = np.empty((H, W), dtype=dtype)
-    fill_host(grid, 2 if dtype == "int32" else 1, 2)
-    out = np.empty_like(grid)
+    kind, seed = INPUTS[args.config]
+    grid = np.concatenate([O.fill((H1, W), dtype, kind, seed + p) for p in range(world)]) \
+        if args.scaling == "weak" else O.fill((H, W), dtype, kind, seed)
+    out = np.zeros_like(grid)
     d = O.desc_from(op, dtype, n, s, e, w, border, pad)
-    per_step = 1  # one generation of the full grid per step (bounded sample)
 
-    def step():
+    def gens(k):
         nonlocal grid, out
-        for _ in range(per_step):
-            O.lib().oracle_stencil(ctypes.byref(d), grid.ctypes.data, out.ctypes.data, W, H, W, W,
-                                   0, 0, threads)
+        rc = O.lib().oracle_baseline_iterate(ctypes.byref(d), grid.ctypes.data, out.ctypes.data,
+                                             W, H, k, threads)
+        assert rc == 0
+        if k % 2:
             grid, out = out, grid
 
+    # bounded sample: the full step (all `iters` generations) when it takes
+    # under ~3 s on this host, else as many generations as fit
+    t0 = time.perf_counter()
+    gens(1)
+    t1 = time.perf_counter() - t0
+    per_step = iters if t1 * iters <= 3.0 else max(1, int(3.0 / max(t1, 1e-6)))
     for _ in range(args.warmup):
-        step()
+        gens(per_step)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        gens(per_step)
     dt = time.perf_counter() - t0
     v = float(H) * W * per_step * args.steps / dt / 1e9
+    sample = (f"{per_step} of {iters} generations of {W}x{H} per step" if per_step < iters
+              else f"the full step: {iters} generations of {W}x{H}")
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": "Gcells/s", "impl": "reference",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (reference Rng stream, seeded)",
-        "config": {"workload": f"{args.config} {W}x{H}, {dtype}, {border} {pad}; each step one "
-                               f"generation of the {iters}-generation workload",
-                   "parallelism": f"{threads} host threads"},
+        "config": workload_config(args.config, world, args.scaling),
         "cpu_baseline": {"value": round(v, 4), "unit": "Gcells/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{per_step} generation(s) of {W}x{H} per step"},
+                         "kind": "port", "sample": sample,
+                         "implementation": "oracle/stencil_oracle.c oracle_baseline_iterate "
+                                           f"({threads} host threads)"},
         "e2e": {"value": round(v, 4), "unit": "Gcells/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_distributed(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous)."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -660,6 +967,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-temporal", action="store_true",
                     help="skip the temporally blocked leg (TB generations per launch)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the lines for the other BASELINE configs (1, 3, 4)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: exchange halos between passes instead of behind the interior")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
@@ -672,6 +981,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

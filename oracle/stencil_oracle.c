@@ -348,9 +348,169 @@ static int check_desc(const oracle_desc* d) {
   return 0;
 }
 
-int oracle_stencil(const oracle_desc* d, const void* in, void* out, int64_t width,
-                   int64_t height, int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
-                   int64_t rows_below, int32_t threads) {
+/* ------------------------------------------------------------ input fill */
+/* std::mt19937_64 (the reference Rng engine, include/wgtune/rng.hpp:34-72). */
+typedef struct {
+  uint64_t mt[312];
+  int i;
+} mt64;
+
+static void mt64_seed(mt64* m, uint64_t seed) {
+  m->mt[0] = seed;
+  for (int k = 1; k < 312; ++k)
+    m->mt[k] = 6364136223846793005ULL * (m->mt[k - 1] ^ (m->mt[k - 1] >> 62)) + (uint64_t)k;
+  m->i = 312;
+}
+
+static uint64_t mt64_next(mt64* m) {
+  if (m->i >= 312) {
+    for (int k = 0; k < 312; ++k) {
+      uint64_t x = (m->mt[k] & 0xFFFFFFFF80000000ULL) | (m->mt[(k + 1) % 312] & 0x7FFFFFFFULL);
+      uint64_t xa = x >> 1;
+      if (x & 1) xa ^= 0xB5026F5AA96619E9ULL;
+      m->mt[k] = m->mt[(k + 156) % 312] ^ xa;
+    }
+    m->i = 0;
+  }
+  uint64_t x = m->mt[m->i++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= x >> 43;
+  return x;
+}
+
+int oracle_fill(int32_t dtype, int32_t kind, uint64_t seed, void* out, int64_t count) {
+  if (!out || count < 0 || dtype < DT_I32 || dtype > DT_F64 || kind < 0 || kind > 3) return -1;
+  mt64* m = (mt64*)malloc(sizeof(mt64));
+  if (!m) return -1;
+  mt64_seed(m, seed);
+  for (int64_t i = 0; i < count; ++i) {
+    double u = (double)(mt64_next(m) >> 11) * 0x1.0p-53;
+    double v = kind == 0 ? 2.0 * u - 1.0 : kind == 1 ? u : kind == 2 ? (u < 0.5 ? 1.0 : 0.0)
+                                                                     : floor(256.0 * u);
+    if (dtype == DT_I32) ((int32_t*)out)[i] = (int32_t)v;
+    else if (dtype == DT_F32) ((float*)out)[i] = (float)v;
+    else ((double*)out)[i] = v;
+  }
+  free(m);
+  return 0;
+}
+
+/* ------------------------------------------------------- CPU baseline path */
+/* Interior rows with the op switch hoisted: plain loops over a row that gcc
+ * vectorises (avx2 clone where the host has it).  Same expressions, same
+ * order, no contraction: bit-identical to cell_*. */
+#define SK_CLONES __attribute__((target_clones("avx2", "default")))
+
+SK_CLONES static void row_gol_i32(const int32_t* up, const int32_t* mid, const int32_t* dn,
+                                  int32_t* out, int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c < c1; ++c) {
+    int n = (up[c - 1] != 0) + (up[c] != 0) + (up[c + 1] != 0) + (mid[c - 1] != 0) +
+            (mid[c + 1] != 0) + (dn[c - 1] != 0) + (dn[c] != 0) + (dn[c + 1] != 0);
+    int alive = mid[c] != 0;
+    out[c] = (n == 3) | (alive & (n == 2));
+  }
+}
+
+SK_CLONES static void row_heat_f32(const float* up, const float* mid, const float* dn, float* out,
+                                   int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c < c1; ++c) {
+    float u = mid[c];
+    float lap = up[c] + dn[c];
+    lap = lap + mid[c + 1];
+    lap = lap + mid[c - 1];
+    lap = lap - 4.0f * u;
+    out[c] = u + 0.2f * lap;
+  }
+}
+
+SK_CLONES static void row_five_f32(const float* up, const float* mid, const float* dn, float* out,
+                                   int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c < c1; ++c) {
+    float s = up[c] + dn[c];
+    s = s + mid[c + 1];
+    s = s + mid[c - 1];
+    s = s + mid[c];
+    out[c] = s * 0.2f;
+  }
+}
+
+/* boxmean f32 over rows r-N..r+S: each row summed west->east, the row sums
+ * north->south, then one division (cell_f32's OP_BOXMEAN order). */
+SK_CLONES static void row_boxmean_f32(const float* in, int64_t pitch, const oracle_desc* d,
+                                      float* out, float* acc, float* row, int64_t c0, int64_t c1) {
+  const float cnt = (float)((d->north + d->south + 1) * (d->east + d->west + 1));
+  for (int dr = -d->north; dr <= d->south; ++dr) {
+    const float* p = in + dr * pitch;
+    for (int64_t c = c0; c < c1; ++c) row[c] = p[c - d->west];
+    for (int dc = -d->west + 1; dc <= d->east; ++dc)
+      for (int64_t c = c0; c < c1; ++c) row[c] = row[c] + p[c + dc];
+    if (dr == -d->north)
+      for (int64_t c = c0; c < c1; ++c) acc[c] = row[c];
+    else
+      for (int64_t c = c0; c < c1; ++c) acc[c] = acc[c] + row[c];
+  }
+  for (int64_t c = c0; c < c1; ++c) out[c] = acc[c] / cnt;
+}
+
+static int fast_op(const oracle_desc* d) {
+  int unit = d->north == 1 && d->south == 1 && d->east == 1 && d->west == 1;
+  if (d->op == OP_GOL && d->dtype == DT_I32 && unit) return 1;
+  if (d->op == OP_HEAT && d->dtype == DT_F32 && unit) return 2;
+  if (d->op == OP_FIVE_POINT && d->dtype == DT_F32 && unit) return 3;
+  if (d->op == OP_BOXMEAN && d->dtype == DT_F32) return 4;
+  return 0;
+}
+
+static void cell_store(const job* j, int64_t r, int64_t c) {
+  switch (j->d->dtype) {
+    case DT_F32: ((float*)j->out)[r * j->pout + c] = cell_f32(j, r, c); break;
+    case DT_F64: ((double*)j->out)[r * j->pout + c] = cell_f64(j, r, c); break;
+    default: ((int32_t*)j->out)[r * j->pout + c] = cell_i32(j, r, c); break;
+  }
+}
+
+static void* run_rows_baseline(void* arg) {
+  job* j = (job*)arg;
+  const oracle_desc* d = j->d;
+  const int kind = fast_op(d);
+  const int64_t cl = d->west, ch = j->W - d->east; /* interior columns [cl, ch) */
+  float *acc = NULL, *row = NULL;
+  if (kind == 4) {
+    acc = (float*)malloc(sizeof(float) * (size_t)j->W);
+    row = (float*)malloc(sizeof(float) * (size_t)j->W);
+  }
+  for (int64_t r = j->r_begin; r < j->r_end; ++r) {
+    const int interior = kind && (kind != 4 || (acc && row)) && r - d->north >= 0 &&
+                         r + d->south <= j->H - 1 && ch > cl;
+    if (!interior) {
+      for (int64_t c = 0; c < j->W; ++c) cell_store(j, r, c);
+      continue;
+    }
+    for (int64_t c = 0; c < cl; ++c) cell_store(j, r, c);
+    for (int64_t c = ch; c < j->W; ++c) cell_store(j, r, c);
+    if (kind == 1) {
+      const int32_t* m = (const int32_t*)j->in + r * j->pin;
+      row_gol_i32(m - j->pin, m, m + j->pin, (int32_t*)j->out + r * j->pout, cl, ch);
+    } else if (kind == 2 || kind == 3) {
+      const float* m = (const float*)j->in + r * j->pin;
+      float* o = (float*)j->out + r * j->pout;
+      if (kind == 2) row_heat_f32(m - j->pin, m, m + j->pin, o, cl, ch);
+      else row_five_f32(m - j->pin, m, m + j->pin, o, cl, ch);
+    } else {
+      row_boxmean_f32((const float*)j->in + r * j->pin, j->pin, d, (float*)j->out + r * j->pout,
+                      acc, row, cl, ch);
+    }
+  }
+  free(acc);
+  free(row);
+  return NULL;
+}
+
+static int run_jobs(const oracle_desc* d, const void* in, void* out, int64_t width,
+                    int64_t height, int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
+                    int64_t rows_below, int32_t threads, void* (*fn)(void*)) {
   if (check_desc(d) || !in || !out || width < 1 || height < 1) return -1;
   if (pitch_in < width || pitch_out < width || rows_above < 0 || rows_below < 0) return -1;
   int nt = threads < 1 ? 1 : threads;
@@ -388,11 +548,37 @@ int oracle_stencil(const oracle_desc* d, const void* in, void* out, int64_t widt
     jobs[t].r_begin = height * t / nt;
     jobs[t].r_end = height * (t + 1) / nt;
   }
-  for (int t = 1; t < nt; ++t) pthread_create(&tids[t], NULL, run_rows, &jobs[t]);
-  run_rows(&jobs[0]);
+  for (int t = 1; t < nt; ++t) pthread_create(&tids[t], NULL, fn, &jobs[t]);
+  fn(&jobs[0]);
   for (int t = 1; t < nt; ++t) pthread_join(tids[t], NULL);
   free(jobs);
   free(tids);
+  return 0;
+}
+
+int oracle_stencil(const oracle_desc* d, const void* in, void* out, int64_t width,
+                   int64_t height, int64_t pitch_in, int64_t pitch_out, int64_t rows_above,
+                   int64_t rows_below, int32_t threads) {
+  return run_jobs(d, in, out, width, height, pitch_in, pitch_out, rows_above, rows_below, threads,
+                  run_rows);
+}
+
+int oracle_baseline_stencil(const oracle_desc* d, const void* in, void* out, int64_t width,
+                            int64_t height, int32_t threads) {
+  return run_jobs(d, in, out, width, height, width, width, 0, 0, threads, run_rows_baseline);
+}
+
+int oracle_baseline_iterate(const oracle_desc* d, void* a, void* b, int64_t width, int64_t height,
+                            int32_t iterations, int32_t threads) {
+  void* src = a;
+  void* dst = b;
+  for (int i = 0; i < iterations; ++i) {
+    int rc = oracle_baseline_stencil(d, src, dst, width, height, threads);
+    if (rc) return rc;
+    void* t = src;
+    src = dst;
+    dst = t;
+  }
   return 0;
 }
 

@@ -50,6 +50,26 @@ int oracle_stencil(const oracle_desc* d, const void* in, void* out, int64_t widt
 int oracle_iterate(const oracle_desc* d, void* a, void* b, int64_t width, int64_t height,
                    int32_t iterations, int32_t threads);
 
+/* Seeded synthetic input with the reference Rng stream (rng.hpp:34-72):
+ * std::mt19937_64(seed), uniform01 = (x >> 11) * 2^-53; kind 0 -> 2u-1,
+ * 1 -> u, 2 -> (u < 0.5), 3 -> floor(256u); cast to dtype (0 i32, 1 f32,
+ * 2 f64).  Mirrors sk_fill_host so CPU-only code (the reference arm) can make
+ * the bench's inputs without loading the product library. */
+int oracle_fill(int32_t dtype, int32_t kind, uint64_t seed, void* out, int64_t count);
+
+/* The CPU BASELINE (timed by bench.py; still test infrastructure): the same
+ * arithmetic as oracle_stencil, but with the op switch hoisted out of the
+ * interior so the compiler vectorises rows (gol/i32, heat/f32,
+ * five_point/f32, boxmean/f32; every other op, the border rows and border
+ * columns go through the per-cell restatement).  Bit-identical to
+ * oracle_stencil (tests/test_oracle_kat.py).  No row-shard halos. */
+int oracle_baseline_stencil(const oracle_desc* d, const void* in, void* out, int64_t width,
+                            int64_t height, int32_t threads);
+
+/* `iterations` baseline passes ping-ponging a <-> b (result as oracle_iterate). */
+int oracle_baseline_iterate(const oracle_desc* d, void* a, void* b, int64_t width, int64_t height,
+                            int32_t iterations, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

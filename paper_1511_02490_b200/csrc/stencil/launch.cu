@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <set>
 #include <thread>
 
 #include "launch_internal.cuh"
@@ -567,8 +568,6 @@ struct Scratch {
   size_t dev_bytes = 0;
   void* diff = nullptr;
   std::vector<cudaEvent_t> events;
-  void* bits[2] = {nullptr, nullptr};  // packed bit grids of the chained gol path
-  size_t bits_bytes = 0;
   // streamed host jobs (sk_stencil_submit_host): three slots, each with its
   // own stream, device ping-pong buffers and completion event, so job j+1's
   // H2D, job j's passes and job j-1's D2H can all be in flight at once
@@ -607,25 +606,35 @@ int scratch(Scratch** out) {
   return SK_OK;
 }
 
-// Packed ping-pong grids of the bit-plane path (per device and thread, kept
-// and grown as needed; freed with the process).
-int scratch_bits(long long words, void** p0, void** p1) {
-  Scratch* s = nullptr;
-  if (int rc = scratch(&s)) return rc;
-  const size_t need = static_cast<size_t>(words) * 4;
-  if (s->bits_bytes < need) {
-    cudaFree(s->bits[0]);
-    cudaFree(s->bits[1]);
-    s->bits[0] = s->bits[1] = nullptr;
-    s->bits_bytes = 0;
-    if (cudaMalloc(&s->bits[0], need) != cudaSuccess || cudaMalloc(&s->bits[1], need) != cudaSuccess) {
-      return fail(SK_ECUDA, "bit-grid scratch allocation failed (%zu B)", need);
+int StreamBits::alloc(size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SK_ECUDA, "cudaGetDevice failed");
+  {
+    static std::mutex mu;
+    static std::set<int> retained;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!retained.count(dev)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      retained.insert(dev);
     }
-    s->bits_bytes = need;
   }
-  *p0 = s->bits[0];
-  *p1 = s->bits[1];
+  for (void*& q : p) {
+    if (cudaMallocAsync(&q, bytes, stream) != cudaSuccess) {
+      q = nullptr;
+      return fail(SK_ECUDA, "bit-grid allocation failed (%zu B)", bytes);
+    }
+  }
   return SK_OK;
+}
+
+StreamBits::~StreamBits() {
+  for (void* q : p) {
+    if (q) cudaFreeAsync(q, stream);
+  }
 }
 
 // Word-wise device comparison; *diff counts differing 16-B words.

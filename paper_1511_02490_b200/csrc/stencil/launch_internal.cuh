@@ -133,7 +133,18 @@ int run_cross(const sk_stencil_desc& d, const void* in, void* out, long long W, 
 
 // --------------------------------------------- per-thread scratch (launch.cu)
 // Packed ping-pong grids of the bit-plane path, grown as needed.
-int scratch_bits(long long words, void** p0, void** p1);
+// Two packed bit grids of the bit-plane path, stream-ordered
+// (cudaMallocAsync / cudaFreeAsync on `stream`, from the device's default
+// pool, which is set to retain its memory so repeated calls do not remap).
+struct StreamBits {
+  cudaStream_t stream;
+  void* p[2] = {nullptr, nullptr};
+  explicit StreamBits(cudaStream_t s) : stream(s) {}
+  int alloc(size_t bytes);
+  ~StreamBits();
+  StreamBits(const StreamBits&) = delete;
+  StreamBits& operator=(const StreamBits&) = delete;
+};
 
 // ------------------------------------------------------- op parameters
 inline long long binom(int n, int k) {

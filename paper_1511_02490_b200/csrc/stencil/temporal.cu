@@ -101,8 +101,12 @@ int run_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, l
   }
   if (iterations == 0) return SK_OK;
   const long long pw = (first.g.nwords + 3) / 4 * 4;  // 16-B packed rows
-  void* P[2] = {nullptr, nullptr};
-  if (int rc = scratch_bits(pw * (H + a + b), &P[0], &P[1])) return rc;
+  // Packed ping-pong grids, allocated stream-ordered on the caller's stream
+  // and freed on it when this call's launches are enqueued: concurrent calls
+  // on different streams (streamed host jobs, user streams) never share them.
+  StreamBits bits(stream);
+  if (int rc = bits.alloc(static_cast<size_t>(pw * (H + a + b)) * 4)) return rc;
+  void* P[2] = {bits.p[0], bits.p[1]};
   DeviceInfo info;
   if (int rc = current_device_info(&info)) return rc;
   const int cvt_grid = 4 * info.sms * 8;  // 8 warps per block, grid-stride

@@ -138,8 +138,22 @@ def iterate_sharded(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iteration
     return src
 
 
+def _one_generation_per_launch(stencil) -> None:
+    """The NCCL schedules exchange N/S-deep halos once per launch, so a
+    launch must advance exactly one generation: a temporally blocked
+    descriptor (TB > 1 generations per launch) would read rows beyond the
+    halo as border and silently change the result.  (The peer schedule,
+    sk_stencil_iterate_peer, runs TB > 1 on the strip path with TB-deep
+    halos.)"""
+    tb = int(getattr(stencil.desc, "fused_iterations", 0)) if hasattr(stencil, "desc") else 0
+    if tb > 1:
+        raise ValueError(f"fused_iterations={tb}: the NCCL row-shard schedule needs one "
+                         "generation per launch (use iterate_sharded_peer for TB > 1)")
+
+
 def cuda_step(stencil, wc: int, wr: int) -> StepFn:
     """Production step: one sm_100a executor launch on the current stream."""
+    _one_generation_per_launch(stencil)
 
     def step(src: torch.Tensor, dst: torch.Tensor, shard: RowShard) -> None:
         stencil(src[shard.north:], dst[shard.north:], wc, wr, rows_above=shard.rows_above,
@@ -163,6 +177,7 @@ def iterate_sharded_overlapped(a: torch.Tensor, b: torch.Tensor, shard: RowShard
     boundary strips wait for that exchange.  Bit-identical to
     iterate_sharded."""
     shard.check()
+    _one_generation_per_launch(stencil)
     n, s, h = shard.north, shard.south, shard.rows
     m = max(n, s)
     if h < 2 * max(m, 1) or shard.world == 1:

@@ -121,6 +121,43 @@ class Stencil:
             raise IllegalWorkgroupSize(msg)
         raise N.NativeError(code, where, N.last_error())
 
+    # -- argument checks (the C side copies / reads W*H*sizeof(T) per buffer)
+    _TORCH_NAMES = {N.SK_INT32: "int32", N.SK_FLOAT32: "float32", N.SK_FLOAT64: "float64"}
+
+    def _check_device(self, *tensors) -> None:
+        want = self._TORCH_NAMES[self._desc.dtype]
+        shape = None
+        for t in tensors:
+            if not getattr(t, "is_cuda", False):
+                raise ValueError("stencil buffers must be CUDA tensors")
+            if str(t.dtype).split(".")[-1] != want:
+                raise ValueError(f"buffer dtype {t.dtype} does not match the stencil's {want}")
+            if t.dim() != 2 or t.stride(1) != 1:
+                raise ValueError("stencil buffers must be 2-D with unit column stride")
+            if shape is not None and t.shape[1] != shape[1]:
+                raise ValueError(f"buffer widths differ: {tuple(t.shape)} vs {shape}")
+            shape = tuple(t.shape)
+
+    def _check_host(self, h_in, h_out) -> None:
+        import numpy as np
+
+        want = np.dtype(self._TORCH_NAMES[self._desc.dtype])
+        for a in (h_in, h_out):
+            if hasattr(a, "data_ptr"):
+                if a.is_cuda or not a.is_contiguous():
+                    raise ValueError("host buffers must be contiguous CPU tensors")
+                dt = np.dtype(str(a.dtype).split(".")[-1])
+            else:
+                if not a.flags["C_CONTIGUOUS"]:
+                    raise ValueError("host buffers must be C-contiguous")
+                dt = np.dtype(a.dtype)
+            if dt != want:
+                raise ValueError(f"host buffer dtype {dt} does not match the stencil's {want}")
+            if len(a.shape) != 2:
+                raise ValueError("host buffers must be 2-D")
+        if tuple(h_in.shape) != tuple(h_out.shape):
+            raise ValueError(f"host buffer shapes differ: {tuple(h_in.shape)} vs {tuple(h_out.shape)}")
+
     def launch_ptr(self, d_in: int, d_out: int, width: int, height: int, pitch_in: int,
                    pitch_out: int, wc: int, wr: int, rows_above: int = 0, rows_below: int = 0,
                    stream: int = 0) -> None:
@@ -135,7 +172,12 @@ class Stencil:
         """One pass from torch tensor ``inp`` to ``out`` (row 0 of both at [0])."""
         import torch
 
+        self._check_device(inp, out)
         h = out.shape[0] if height is None else height
+        # rows_above halo rows sit before inp's first row (not checkable here)
+        if h < 0 or h > out.shape[0] or rows_above < 0 or rows_below < 0 or \
+                inp.shape[0] < h + rows_below:
+            raise ValueError("height / halo rows exceed the buffers")
         s = (stream or torch.cuda.current_stream(inp.device)).cuda_stream
         self.launch_ptr(inp.data_ptr(), out.data_ptr(), out.shape[1], h, inp.stride(0),
                         out.stride(0), wc, wr, rows_above, rows_below, s)
@@ -144,6 +186,9 @@ class Stencil:
         """``iterations`` ping-pong passes; returns the tensor holding the result."""
         import torch
 
+        self._check_device(a, b)
+        if tuple(a.shape) != tuple(b.shape) or a.stride(0) != b.stride(0):
+            raise ValueError("iterate needs two buffers of the same shape and pitch")
         s = (stream or torch.cuda.current_stream(a.device)).cuda_stream
         in_b = ctypes.c_int32(0)
         rc = N.lib().sk_stencil_iterate(ctypes.byref(self._desc), a.data_ptr(), b.data_ptr(),
@@ -174,6 +219,9 @@ class Stencil:
     def time(self, inp, out, wc: int, wr: int, samples: int = 30, warmup: int = 3,
              flush_l2: bool = True) -> list[float]:
         """``samples`` cudaEvent-timed passes (ms), after ``warmup`` untimed ones."""
+        self._check_device(inp, out)
+        if inp.shape[0] < out.shape[0]:
+            raise ValueError("input has fewer rows than the output")
         ms = (ctypes.c_double * max(samples, 1))()
         rc = N.lib().sk_stencil_time(ctypes.byref(self._desc), inp.data_ptr(), out.data_ptr(),
                                      out.shape[1], out.shape[0], inp.stride(0), wc, wr, warmup,
@@ -184,6 +232,7 @@ class Stencil:
 
     def run_host(self, h_in, h_out, iterations: int, wc: int, wr: int) -> None:
         """End-to-end from host arrays (numpy or pinned torch CPU tensors)."""
+        self._check_host(h_in, h_out)
         pin = _host_ptr(h_in)
         pout = _host_ptr(h_out)
         height, width = h_in.shape
@@ -196,6 +245,7 @@ class Stencil:
     def submit_host(self, h_in, h_out, iterations: int, wc: int, wr: int) -> int:
         """Streamed end-to-end job (pinned host buffers): returns a ticket
         immediately; at most three jobs are in flight per thread."""
+        self._check_host(h_in, h_out)
         t = ctypes.c_int64(-1)
         height, width = h_in.shape
         rc = N.lib().sk_stencil_submit_host(ctypes.byref(self._desc), _host_ptr(h_in),

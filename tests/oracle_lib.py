@@ -44,7 +44,45 @@ def lib():
         _lib.oracle_iterate.argtypes = [ctypes.POINTER(oracle_desc), ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int32, ctypes.c_int32]
+        _lib.oracle_fill.restype = ctypes.c_int
+        _lib.oracle_fill.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                     ctypes.c_void_p, ctypes.c_int64]
+        _lib.oracle_baseline_stencil.restype = ctypes.c_int
+        _lib.oracle_baseline_stencil.argtypes = [ctypes.POINTER(oracle_desc), ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                                 ctypes.c_int32]
+        _lib.oracle_baseline_iterate.restype = ctypes.c_int
+        _lib.oracle_baseline_iterate.argtypes = _lib.oracle_iterate.argtypes
     return _lib
+
+
+def fill(shape, dtype, kind: int, seed: int) -> np.ndarray:
+    """The bench/test input stream (reference Rng, mt19937_64) without the
+    product library: kind 0 -> 2u-1, 1 -> u, 2 -> u<0.5, 3 -> floor(256u)."""
+    a = np.empty(shape, dtype=dtype)
+    rc = lib().oracle_fill(DT[np.dtype(dtype)], kind, seed, a.ctypes.data, a.size)
+    assert rc == 0, "oracle_fill rejected arguments"
+    return a
+
+
+def baseline_stencil(desc: oracle_desc, grid: np.ndarray, threads: int = 8) -> np.ndarray:
+    """One pass of the vectorised CPU baseline (bit-identical to stencil())."""
+    grid = np.ascontiguousarray(grid)
+    out = np.empty_like(grid)
+    rc = lib().oracle_baseline_stencil(ctypes.byref(desc), grid.ctypes.data, out.ctypes.data,
+                                       grid.shape[1], grid.shape[0], threads)
+    assert rc == 0
+    return out
+
+
+def baseline_iterate(desc: oracle_desc, grid: np.ndarray, iterations: int,
+                     threads: int = 8) -> np.ndarray:
+    a = np.ascontiguousarray(grid).copy()
+    b = np.empty_like(a)
+    rc = lib().oracle_baseline_iterate(ctypes.byref(desc), a.ctypes.data, b.ctypes.data,
+                                       a.shape[1], a.shape[0], iterations, threads)
+    assert rc == 0
+    return b if iterations % 2 else a
 
 
 def desc_from(op, dtype, n=1, s=1, e=1, w=1, border="pad", pad=0.0, complexity=0,

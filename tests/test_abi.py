@@ -44,6 +44,21 @@ def test_fill_host_matches_reference_rng():
     assert a[0] == (14514284786278117030 >> 11) * 2.0 ** -53
 
 
+def test_fill_host_equals_oracle_fill():
+    # the bench's GPU arm fills through the product library, the reference
+    # arm through oracle_fill: the two streams must be identical
+    import numpy as np
+
+    import oracle_lib as O
+    from paper_1511_02490_b200 import fill_host
+
+    for dtype in ("int32", "float32", "float64"):
+        for kind in range(4):
+            a = np.empty((37, 41), dtype)
+            fill_host(a, kind, 1000 + kind)
+            assert a.tobytes() == O.fill((37, 41), dtype, kind, 1000 + kind).tobytes()
+
+
 def test_invalid_descriptor_is_einval_without_gpu():
     d = N.sk_stencil_desc(op=99, dtype=1)
     km = ctypes.c_int32(0)

@@ -120,3 +120,21 @@ def test_rowshard_geometry():
     assert shards[1].buffer_rows == 2 + 33 + 1
     with pytest.raises(ValueError):
         RowShard(4, 8, 0, 4, 2, 2).check()
+
+
+def test_nccl_schedules_reject_temporal_blocking():
+    """one launch of a TB > 1 descriptor advances TB generations,
+    but the NCCL schedules only exchange N/S-deep halos per launch."""
+    import pytest
+
+    from paper_1511_02490_b200 import Stencil
+    from paper_1511_02490_b200.distributed import RowShard, cuda_step, iterate_sharded_overlapped
+
+    st = Stencil(op="heat", dtype="float32", load_path="strips", fused_iterations=4)
+    with pytest.raises(ValueError, match="fused_iterations"):
+        cuda_step(st, 32, 8)
+    shard = RowShard(64, 32, 0, 2, 1, 1)
+    a = torch.zeros((shard.buffer_rows, 32))
+    with pytest.raises(ValueError, match="fused_iterations"):
+        iterate_sharded_overlapped(a, a.clone(), shard, 3, st, 32, 8)
+    cuda_step(Stencil(op="heat", dtype="float32"), 32, 8)  # one generation per launch: fine

@@ -134,3 +134,48 @@ def test_oracle_matches_numpy_golden(name):
         out = O.stencil(d, x, threads=threads)
         assert out.dtype == y.dtype
         assert out.tobytes() == y.tobytes(), f"{name}: oracle differs from numpy golden"
+
+
+# ----------------------------------------------------------- input + baseline
+def test_oracle_fill_matches_mt19937_64():
+    # std::mt19937_64 default seed 5489: 10000th output is 9981545732273789042
+    # (C++11 [rand.predef]); first output 14514284786278117030.
+    a = O.fill((4,), "float64", 1, 5489)
+    assert a[0] == (14514284786278117030 >> 11) * 2.0 ** -53
+    b = O.fill((10000,), "float64", 1, 5489)
+    assert b[-1] == (9981545732273789042 >> 11) * 2.0 ** -53
+    g = O.fill((64, 64), "int32", 2, 2)
+    assert set(np.unique(g)) <= {0, 1} and 1500 < g.sum() < 2600
+    f = O.fill((1000,), "float32", 0, 1)
+    assert f.min() >= -1.0 and f.max() <= 1.0
+
+
+@pytest.mark.parametrize("op,dtype,borders,border,pad", [
+    ("gol", "int32", (1, 1, 1, 1), "pad", 0.0),
+    ("gol", "int32", (1, 1, 1, 1), "nearest", 0.0),
+    ("heat", "float32", (1, 1, 1, 1), "nearest", 0.0),
+    ("heat", "float32", (1, 1, 1, 1), "pad", 0.5),
+    ("five_point", "float32", (1, 1, 1, 1), "pad", 0.0),
+    ("five_point", "float32", (1, 1, 1, 1), "pad", 1.0),
+    ("boxmean", "float32", (5, 1, 3, 0), "nearest", 0.0),
+    ("boxmean", "float32", (2, 3, 0, 4), "pad", -1.5),
+    ("sobel", "float32", (1, 1, 1, 1), "nearest", 0.0),   # no fast path: per-cell
+    ("heat", "float64", (1, 1, 1, 1), "nearest", 0.0),
+])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 9), (7, 3), (37, 129), (130, 67)])
+def test_baseline_is_bit_identical_to_oracle(op, dtype, borders, border, pad, shape):
+    n, s, e, w = borders
+    d = O.desc_from(op, dtype, n, s, e, w, border, pad)
+    kind = 2 if op == "gol" else 0
+    g = O.fill(shape, dtype, kind, 11 + shape[0])
+    want = O.iterate(d, g, 3, threads=3)
+    got = O.baseline_iterate(d, g, 3, threads=3)
+    assert got.tobytes() == want.tobytes()
+
+
+def test_baseline_special_values_bit_identical():
+    d = O.desc_from("heat", "float32", border="nearest")
+    g = O.fill((33, 70), "float32", 0, 4)
+    g[3, 5], g[10, 10], g[20, 30] = np.inf, -np.nan, -0.0
+    g[5, 6] = 1e-40  # subnormal
+    assert O.baseline_stencil(d, g).tobytes() == O.stencil(d, g).tobytes()

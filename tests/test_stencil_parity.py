@@ -395,3 +395,39 @@ def test_boxmean_division_special_values(path):
     torch.cuda.synchronize()
     want = O.stencil(O.desc_from_stencil(st), x)
     assert b.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
+def test_streamed_bitplane_gol_jobs_and_concurrent_streams():
+    """the bit-plane path's packed grids used to be one
+    buffer pair per (device, thread), shared by the three streamed job slots
+    and by user streams.  Three bit-plane GoL jobs in flight, and two
+    iterate() calls on different user streams from one thread, must each
+    equal the CPU oracle."""
+    import torch
+
+    st = Stencil(op="gol", dtype="int32", load_path="bitplane", fused_iterations=8)
+    rng = np.random.default_rng(21)
+    jobs = [((rng.random((700, 1031)) < 0.45).astype(np.int32), 37) for _ in range(6)]
+    ins = [torch.from_numpy(x).pin_memory() for x, _ in jobs]
+    outs = [torch.empty_like(t).pin_memory() for t in ins]
+    tickets = []
+    for (x, it), hi, ho in zip(jobs, ins, outs):
+        if len(tickets) >= 3:
+            st.wait_host(tickets[-3])
+        tickets.append(st.submit_host(hi, ho, it, 32, 8))
+    for t in tickets:
+        st.wait_host(t)
+    for (x, it), ho in zip(jobs, outs):
+        assert ho.numpy().tobytes() == O.iterate(O.desc_from_stencil(st), x, it).tobytes()
+    # two user streams, launches interleaved from one thread
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    xs = [torch.from_numpy(x).cuda() for x, _ in jobs[:2]]
+    torch.cuda.synchronize()
+    res = []
+    for x, s in zip(xs, (s1, s2)):
+        with torch.cuda.stream(s):
+            res.append(st.iterate(x, torch.empty_like(x), 45, 32, 8, stream=s))
+    torch.cuda.synchronize()
+    for (x, _), r in zip(jobs[:2], res):
+        assert r.cpu().numpy().tobytes() == O.iterate(O.desc_from_stencil(st), x, 45).tobytes()
