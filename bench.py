@@ -48,7 +48,7 @@ def workload_config(config: str, world: int, scaling: str) -> dict:
     H = H1 * world if scaling == "weak" else H1
     rows = H // world
     es = np.dtype(dtype).itemsize
-    per = "per GPU" if scaling == "weak" else "global"
+    per = "per GPU" if scaling == "weak" else f"global ({W}x{rows} per GPU)"
     return {
         "workload": f"{config} {W}x{H1} {per}, {dtype}, {border} {pad}, {iters} generations/step "
                     f"({BASELINE_LABEL[config]})",

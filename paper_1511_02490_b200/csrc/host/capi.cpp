@@ -1,4 +1,6 @@
 // extern "C" entry points of libwgtb (include/wgtb_c.h).
+#include <cuda_runtime.h>
+
 #include <chrono>
 #include <map>
 #include <memory>
@@ -61,7 +63,9 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
     const wgtb::KernelDescriptor k = wgtb::kernel_from_json(nlohmann::json::parse(wgtb::read_text(kernel_json)));
     wgtb::DatasetDescriptor ds{static_cast<int>(width), static_cast<int>(height), element_of(desc->dtype),
                                element_of(desc->dtype)};
-    const wgtb::Scenario s = wgtb::make_scenario(wgtb::device_from_cuda(0), k, ds);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) throw wgtb::DeviceError("cudaGetDevice failed");
+    const wgtb::Scenario s = wgtb::make_scenario(wgtb::device_from_cuda(dev), k, ds);
     const wgtb::FeatureVector f = wgtb::extract(s);
     int32_t kmax = 0;
     if (sk_kernel_max_wgsize(desc, &kmax) != SK_OK) throw wgtb::DeviceError(sk_last_error());

@@ -33,11 +33,25 @@ int fail(int code, const char* fmt, ...) {
 }
 
 // Launch-time errors that leave the context usable and mean "this
-// configuration cannot run" -> refused parameter.
+// configuration cannot run" -> refused parameter.  Only
+// the two resource/config errors qualify: the dynamic shared-memory
+// attribute is raised to the opt-in maximum when the kernel's attributes are
+// first read, so cudaErrorInvalidValue at launch is a bad argument (a bug),
+// reported as SK_EINVAL rather than hidden as a refused size.
 bool is_config_error(cudaError_t e) {
-  return e == cudaErrorInvalidConfiguration || e == cudaErrorLaunchOutOfResources ||
-         e == cudaErrorInvalidValue ||
-         e == cudaErrorSharedObjectInitFailed;
+  return e == cudaErrorInvalidConfiguration || e == cudaErrorLaunchOutOfResources;
+}
+
+int launch_error(cudaError_t e) {
+  if (is_config_error(e)) {
+    cudaGetLastError();
+    return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
+  }
+  if (e == cudaErrorInvalidValue) {
+    cudaGetLastError();
+    return fail(SK_EINVAL, "launch rejected an argument: %s", cudaGetErrorString(e));
+  }
+  return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
 }
 
 size_t dtype_size(int dtype) { return dtype == SK_FLOAT64 ? 8 : 4; }
@@ -512,8 +526,11 @@ int launch_driver(const Plan& plan, dim3 grid, dim3 block, void** args, cudaStre
                                static_cast<unsigned>(plan.smem), reinterpret_cast<CUstream>(stream), args,
                                nullptr);
   if (r == CUDA_SUCCESS) return SK_OK;
-  if (r == CUDA_ERROR_INVALID_VALUE || r == CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES) {
+  if (r == CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES) {
     return fail(SK_REFUSED, "launch refused (driver error %d)", static_cast<int>(r));
+  }
+  if (r == CUDA_ERROR_INVALID_VALUE) {
+    return fail(SK_EINVAL, "launch rejected an argument (driver error %d)", static_cast<int>(r));
   }
   return fail(SK_ECUDA, "custom kernel launch failed (driver error %d)", static_cast<int>(r));
 }
@@ -521,11 +538,7 @@ int launch_driver(const Plan& plan, dim3 grid, dim3 block, void** args, cudaStre
 int launch_checked(KernelPtr k, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
   cudaError_t e = cudaLaunchKernel(k, grid, block, args, smem, stream);
   if (e == cudaSuccess) return SK_OK;
-  if (is_config_error(e)) {
-    cudaGetLastError();
-    return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
-  }
-  return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  return launch_error(e);
 }
 
 int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, long long H,

@@ -32,6 +32,8 @@ extern thread_local std::string g_last_error;  // sk_last_error()
 extern std::mutex g_mu;                        // guards every cache below
 int fail(int code, const char* fmt, ...);
 bool is_config_error(cudaError_t e);
+// Status for a failed launch: SK_REFUSED / SK_EINVAL / SK_ECUDA.
+int launch_error(cudaError_t e);
 size_t dtype_size(int dtype);
 
 // ---------------------------------------------------------- device facts
@@ -215,13 +217,7 @@ inline int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* 
     e = cudaLaunchKernel(plan.kernel, dim3(plan.g.tiles_x * plan.g.tiles_y), block, args,
                          plan.smem, stream);
   }
-  if (e != cudaSuccess) {
-    if (is_config_error(e)) {
-      cudaGetLastError();
-      return fail(SK_REFUSED, "launch refused: %s", cudaGetErrorString(e));
-    }
-    return fail(SK_ECUDA, "launch failed: %s", cudaGetErrorString(e));
-  }
+  if (e != cudaSuccess) return launch_error(e);
   return SK_OK;
 }
 

@@ -37,7 +37,7 @@ def test_bench_two_ranks_json_line(transport):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_grid"] == "8192x16384"
     assert d["e2e"]["value"] > 0
-    assert ("peer-memory" in d["config"]["parallelism"]) == (transport == "peer")
+    assert (d["transport"] == "peer") == (transport == "peer")
 
 
 def test_bench_two_ranks_heat_temporal_leg():
@@ -48,7 +48,7 @@ def test_bench_two_ranks_heat_temporal_leg():
     lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
     assert proc.returncode == 0 and len(lines) == 1, proc.stdout + proc.stderr[-3000:]
     d = json.loads(lines[0])
-    assert d["config"]["transport"] == "peer"
+    assert d["transport"] == "peer"
     t = d["temporal_blocking"]
     assert t and t["bit_exact_vs_one_pass"] and t["value"] > 0
 
