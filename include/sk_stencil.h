@@ -83,13 +83,22 @@ typedef enum {
                            fused_iterations >= 2, except K in {1,2,4} with
                            TB in {2,4} (per-cell fused kernel).  Work-item = 32 cells of a
                            row x K rows; tile = wc words x wr*K rows.       */
-  SK_LOAD_STRIPS = 4    /* five_point / heat with N=S=E=W=1 only: register
+  SK_LOAD_STRIPS = 4,   /* five_point / heat with N=S=E=W=1 only: register
                            strips, any TB in [1, 32] generations per launch;
                            AUTO takes it for those ops when TB > 4.  Work-
                            item = 4 cells of a row x K rows (K in {4, 8, 16},
                            0 = 8, float64 4); the block's tile is 128 columns x
                            (wc*wr/32)*K rows, of which 4(32 - 2 ceil(TB/4))
                            x ((wc*wr/32)*K - 2 TB) are stored.              */
+  SK_LOAD_VECTOR = 5    /* one pass, TMA-staged tile, vector work-items:
+                           V = 16 B / sizeof(T) adjacent cells of a row x K
+                           rows (128-bit shared loads, one 128-bit global
+                           store per row); tile = V*wc x wr*K cells.  For
+                           five_point / heat / gol / sobel / nms with
+                           N=S=E=W=1 and boxmean with (5,1,3,0); one pass
+                           per launch (fused_iterations <= 1); needs 16-B
+                           aligned buffers and pitches; a tile wider than a
+                           TMA box (256 elements) is refused.               */
 } sk_load_path;
 
 /* Stencil descriptor: the kernel half of a reference KernelDescriptor

@@ -26,7 +26,7 @@ DTYPE_NAMES = {SK_INT32: "INT32", SK_FLOAT32: "FLOAT32", SK_FLOAT64: "FLOAT64"}
 DTYPE_SIZE = {SK_INT32: 4, SK_FLOAT32: 4, SK_FLOAT64: 8}
 
 SK_BORDER_PAD, SK_BORDER_NEAREST = 0, 1
-SK_LOAD_AUTO, SK_LOAD_TMA, SK_LOAD_EXPLICIT, SK_LOAD_BITPLANE, SK_LOAD_STRIPS = 0, 1, 2, 3, 4
+SK_LOAD_AUTO, SK_LOAD_TMA, SK_LOAD_EXPLICIT, SK_LOAD_BITPLANE, SK_LOAD_STRIPS, SK_LOAD_VECTOR = 0, 1, 2, 3, 4, 5
 
 # sk_op
 OPS = {

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "ops.cuh"
+#include "vector.cuh"
 
 namespace sk {
 
@@ -55,6 +56,8 @@ struct Geom {
   int N, S, E, Wb;          // border region (Wb = west)
   int wc, wr;               // workgroup (block) shape, threads
   int K;                    // cells per work-item (consecutive rows of one column)
+  int V;                    // columns per work-item (1, or 16 B / sizeof(T) on SK_LOAD_VECTOR)
+  int tile_cols;            // output columns per tile = wc * V
   int tile_rows;            // output rows per tile = wr * K
   int ex_lo, ex_hi;         // tiles with ex_lo <= tx <= ex_hi and
   int ey_lo, ey_hi;         //   ey_lo <= ty <= ey_hi need no border work
@@ -308,7 +311,7 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage,
     ty = peer_tile_row(g, ty);
     peer_wait_rows(g, ty);
   }
-  int x = tx * g.wc - g.Wb;
+  int x = tx * g.tile_cols - g.Wb;
   x -= x & (g.vec - 1);                      // 16-B aligned innermost start
   int y = ty * g.tile_rows - g.N + g.above;  // tensor rows start `above` rows before row 0
   mbar_arrive_expect_tx(bar, static_cast<uint32_t>(g.nchunks * g.box_h * g.tile_w * sizeof(T)));
@@ -317,7 +320,25 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* stage,
   }
 }
 
-template <class Op, typename T, int K, int MAXT, bool PEER = false>
+// V > 1: vector work-items (vector.cuh), V columns x K rows each.
+template <typename T, int K, int V>
+__device__ __forceinline__ void store_row_vec(T* __restrict__ out, const Geom& g, int r, int c, bool edge,
+                                              const T (&v)[V]) {
+  T* dst = out + static_cast<long long>(r) * g.pitch_out + c;
+  if (!edge) {
+    Vec<T, V> x;
+#pragma unroll
+    for (int j = 0; j < V; ++j) x.v[j] = v[j];
+    *reinterpret_cast<Vec<T, V>*>(dst) = x;
+  } else if (r < g.H) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (c + j < g.W) dst[j] = v[j];
+    }
+  }
+}
+
+template <class Op, typename T, int K, int MAXT, bool PEER = false, int V = 1>
 __global__ void __launch_bounds__(MAXT)
     k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
                   const T pad, const __grid_constant__ OpParams<T> p) {
@@ -383,7 +404,7 @@ __global__ void __launch_bounds__(MAXT)
     }
     const int tyr = PEER ? peer_tile_row(g, ty) : ty;  // boundary tile-rows first (PEER)
     const int r0 = tyr * g.tile_rows;
-    const int c0 = tx * g.wc;
+    const int c0 = tx * g.tile_cols;
     const bool edge = tile_is_edge(g, tx, tyr);
     T* tile = reinterpret_cast<T*>(smem + s * g.stage_bytes) + tile_offset(g, c0);
 
@@ -394,13 +415,23 @@ __global__ void __launch_bounds__(MAXT)
       fence_proxy_async_smem();  // generic writes before the next async refill
       __syncthreads();
     }
-    T res[K];
-    compute_tile<Op, T, K>(tile, g, p, res);
-    store_tile<T, K>(out, g, r0, c0, edge, res);
-    if constexpr (PEER) {
-      if (peer_boundary_row(g, tyr)) {
-        const bool stored = store_peer_rows<T, K>(g, r0, c0, res);
-        peer_tile_done(g, tid, stored);
+    if constexpr (V > 1) {
+      // stream the work-item's rows; each output row leaves as one vector
+      const T* first = tile + (threadIdx.y * K + g.N) * g.tile_w + threadIdx.x * V + g.Wb;
+      const int r = r0 + threadIdx.y * K;
+      const int c = c0 + threadIdx.x * V;
+      vector_tile<Op, T, K, V>(first, g.tile_w, p, [&](int k, const T (&v)[V]) {
+        store_row_vec<T, K, V>(out, g, r + k, c, edge, v);
+      });
+    } else {
+      T res[K];
+      compute_tile<Op, T, K>(tile, g, p, res);
+      store_tile<T, K>(out, g, r0, c0, edge, res);
+      if constexpr (PEER) {
+        if (peer_boundary_row(g, tyr)) {
+          const bool stored = store_peer_rows<T, K>(g, r0, c0, res);
+          peer_tile_done(g, tid, stored);
+        }
       }
     }
     // Release the stage only after the stores: they consume every value the
@@ -436,7 +467,7 @@ __global__ void __launch_bounds__(MAXT)
   const int by = blockIdx.x / g.tiles_x;  // 1-D grid of tiles (no 65535 limit)
   const int bx = blockIdx.x - by * g.tiles_x;
   const int r0 = by * g.tile_rows;
-  const int c0 = bx * g.wc;
+  const int c0 = bx * g.tile_cols;
   const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
   const int total = g.tile_h * g.lw;
   const bool edge = tile_is_edge(g, bx, by);

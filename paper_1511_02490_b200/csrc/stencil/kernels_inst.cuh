@@ -17,6 +17,17 @@ KernelPair pair_for() {
 }
 
 template <class Op, typename T>
+KernelPtr vector_for_k(int K) {
+  constexpr int V = 16 / sizeof(T);
+  switch (K) {
+    case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, 1024, false, V>);
+    case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, 1024, false, V>);
+    case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, 1024, false, V>);
+    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, false, V>);
+  }
+}
+
+template <class Op, typename T>
 KernelPtr peer_for_k(int K) {
   switch (K) {
     case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, 1024, true>);
@@ -100,6 +111,25 @@ KernelPtr SK_PEER_FN(const sk_stencil_desc& d, int K) {
         return peer_for_k<BoxMeanFixed<5, 1, 3, 0>, T>(K);
       }
       return peer_for_k<BoxMean, T>(K);
+    default: return nullptr;
+  }
+}
+
+// Vector work-items: only for the border region the op's vector form has.
+KernelPtr SK_VECTOR_FN(const sk_stencil_desc& d, int K) {
+  using T = SK_T;
+  const bool unit = d.north == 1 && d.south == 1 && d.east == 1 && d.west == 1;
+  switch (d.op) {
+    case SK_OP_FIVE_POINT: return unit ? vector_for_k<FivePoint, T>(K) : nullptr;
+    case SK_OP_HEAT: return unit ? vector_for_k<Heat, T>(K) : nullptr;
+    case SK_OP_GOL: return unit ? vector_for_k<Gol, T>(K) : nullptr;
+    case SK_OP_SOBEL: return unit ? vector_for_k<Sobel, T>(K) : nullptr;
+    case SK_OP_NMS: return unit ? vector_for_k<Nms, T>(K) : nullptr;
+    case SK_OP_BOXMEAN:
+      if (d.north == 5 && d.south == 1 && d.east == 3 && d.west == 0) {
+        return vector_for_k<BoxMeanFixed<5, 1, 3, 0>, T>(K);
+      }
+      return nullptr;
     default: return nullptr;
   }
 }

@@ -131,8 +131,11 @@ int validate_desc(const sk_stencil_desc* d) {
   if (d->border_mode != SK_BORDER_PAD && d->border_mode != SK_BORDER_NEAREST) {
     return fail(SK_EINVAL, "bad border mode %d", d->border_mode);
   }
-  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_STRIPS) {
+  if (d->load_path < SK_LOAD_AUTO || d->load_path > SK_LOAD_VECTOR) {
     return fail(SK_EINVAL, "bad load path %d", d->load_path);
+  }
+  if (d->load_path == SK_LOAD_VECTOR && d->fused_iterations > 1) {
+    return fail(SK_ENOTSUP, "the vector path runs one generation per launch (fused_iterations <= 1)");
   }
   if (d->load_path == SK_LOAD_BITPLANE && d->op != SK_OP_GOL) {
     return fail(SK_ENOTSUP, "the bit-plane path is Game of Life only");
@@ -199,6 +202,14 @@ KernelPtr fused_for_desc(const sk_stencil_desc& d, int K, int TB) {
     case SK_INT32: return fused_i32(d, K, TB);
     case SK_FLOAT32: return fused_f32(d, K, TB);
     default: return fused_f64(d, K, TB);
+  }
+}
+
+KernelPtr vector_for_desc(const sk_stencil_desc& d, int K) {
+  switch (d.dtype) {
+    case SK_INT32: return vector_i32(d, K);
+    case SK_FLOAT32: return vector_f32(d, K);
+    default: return vector_f64(d, K);
   }
 }
 
@@ -384,6 +395,17 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
                          : kernels_for_desc(d, K);
   if (!kp.tma || !kp.explicit_) return fail(SK_EINVAL, "kernel table has no entry for K=%d", K);
   const bool drv = custom != nullptr;
+  // vector work-items: V = 16 B of cells per work-item row (vector.cuh)
+  const bool vec_path = !drv && d.load_path == SK_LOAD_VECTOR;
+  int V = 1;
+  if (vec_path) {
+    kp.tma = vector_for_desc(d, K);
+    if (!kp.tma) {
+      return fail(SK_ENOTSUP, "no vector kernel for op %d with border (%d,%d,%d,%d)", d.op, d.north,
+                  d.south, d.east, d.west);
+    }
+    V = static_cast<int>(16 / dtype_size(d.dtype));
+  }
   plan->driver_handle = drv;
   // temporal blocking: TB generations per launch (TMA path only)
   const int TB = (!drv && d.fused_iterations > 1) ? d.fused_iterations : 1;
@@ -418,20 +440,23 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   g.wc = wc;
   g.wr = wr;
   g.K = K;
+  g.V = V;
+  g.tile_cols = wc * V;
+  const int tc = g.tile_cols;
   g.tile_rows = wr * K;
-  g.lw = wc + eE + eW;
+  g.lw = tc + eE + eW;
   const int vec = static_cast<int>(16 / es);
   g.vec = vec;
   // Box width: the logical tile plus the largest 16-B alignment offset any
   // tile can have (constant when wc is a multiple of vec).
-  const int max_off = (wc % vec == 0) ? ((-eW) & (vec - 1)) : vec - 1;
+  const int max_off = (tc % vec == 0) ? ((-eW) & (vec - 1)) : vec - 1;
   g.tile_w = (g.lw + max_off + vec - 1) / vec * vec;
   g.tile_h = g.tile_rows + eN + eS;
-  g.tiles_x = static_cast<int>((W + wc - 1) / wc);
+  g.tiles_x = static_cast<int>((W + tc - 1) / tc);
   g.tiles_y = static_cast<int>((H + g.tile_rows - 1) / g.tile_rows);
   // Interior tiles: read only inside the readable window and store in range.
-  g.ex_lo = static_cast<int>(ceil_div(eW, wc));
-  g.ex_hi = static_cast<int>(floor_div(W - wc - eE, wc));
+  g.ex_lo = static_cast<int>(ceil_div(eW, tc));
+  g.ex_hi = static_cast<int>(floor_div(W - tc - eE, tc));
   g.ey_lo = static_cast<int>(ceil_div(std::max<long long>(0, eN - g.above), g.tile_rows));
   g.ey_hi = static_cast<int>(floor_div(H + g.below - eS - g.tile_rows, g.tile_rows));
   g.mode = d.border_mode;
@@ -449,6 +474,13 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   }
   if (d.load_path == SK_LOAD_TMA && !tma_ok) {
     return fail(SK_ENOTSUP, "TMA path not possible for this tile/buffer (tile_w %d)", g.tile_w);
+  }
+  if (vec_path) {
+    if (g.tile_w > 256) {
+      return fail(SK_REFUSED, "vector tile %d columns wide exceeds one TMA box (256)", g.tile_w);
+    }
+    if (!tma_ok) return fail(SK_ENOTSUP, "the vector path needs 16-B aligned input and pitch");
+    use_tma = true;
   }
   const KernelAttr& attr = use_tma ? a_tma : a_exp;
   plan->kernel_max = std::min(info.max_threads, attr.max_threads);
@@ -780,7 +812,7 @@ int sk_stencil_probe(const sk_stencil_desc* desc, int64_t width, int64_t height,
   int rc = make_plan(*desc, width, height, width, width, 0, 0, wc, wr, nullptr, &plan);
   if (kernel_max) *kernel_max = plan.kernel_max;
   if (tile_bytes) *tile_bytes = plan.tile_bytes;
-  if (load_path) *load_path = plan.tma ? SK_LOAD_TMA : SK_LOAD_EXPLICIT;
+  if (load_path) *load_path = plan.g.V > 1 ? SK_LOAD_VECTOR : plan.tma ? SK_LOAD_TMA : SK_LOAD_EXPLICIT;
   return rc;
 }
 

@@ -188,6 +188,10 @@ inline int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* 
   OpParams<T> p;
   fill_params<T>(d, &p);
   T pad = static_cast<T>(d.pad_value);
+  if (plan.g.V > 1 && ((reinterpret_cast<uintptr_t>(out) % 16) != 0 ||
+                       (plan.g.pitch_out * static_cast<long long>(sizeof(T))) % 16 != 0)) {
+    return fail(SK_EINVAL, "the vector path stores 16 B per row: output and its pitch must be 16-B aligned");
+  }
   dim3 block(plan.g.wc, plan.g.wr, 1);
   cudaError_t e;
   if (plan.tma) {

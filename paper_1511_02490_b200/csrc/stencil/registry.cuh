@@ -14,6 +14,13 @@ struct KernelPair {
   KernelPtr explicit_;
 };
 
+// Vector-work-item one-pass kernels (SK_LOAD_VECTOR, vector.cuh):
+// k_stencil_tma<Op, T, K, 1024, false, 16 / sizeof(T)>; nullptr when the op
+// (with this descriptor's border) has no vector form.
+KernelPtr vector_i32(const sk_stencil_desc& d, int K);
+KernelPtr vector_f32(const sk_stencil_desc& d, int K);
+KernelPtr vector_f64(const sk_stencil_desc& d, int K);
+
 // K in {1, 2, 4, 8}: cells per work-item.
 KernelPair kernels_i32(const sk_stencil_desc& d, int K);
 KernelPair kernels_f32(const sk_stencil_desc& d, int K);

@@ -64,6 +64,8 @@ class Stencil:
     instructions: int = 100      # synthetic kernels only
     load_path: str = "auto"      # "auto" | "tma" | "explicit" | "bitplane" (gol)
                                  # | "strips" (five_point / heat, unit borders)
+                                 # | "vector" (16-B vector work-items: five_point,
+                                 #   heat, gol, sobel, nms unit borders; boxmean 5,1,3,0)
     cells_per_thread: int = 0    # K cells per work-item; 0 = auto
     fused_iterations: int = 0    # temporal blocking: generations per launch
                                  # (0/1, 2, 4; gol on the bit-plane path: 1..128;
@@ -82,7 +84,8 @@ class Stencil:
             load_path={"auto": N.SK_LOAD_AUTO, "tma": N.SK_LOAD_TMA,
                        "explicit": N.SK_LOAD_EXPLICIT,
                        "bitplane": N.SK_LOAD_BITPLANE,
-                       "strips": N.SK_LOAD_STRIPS}[self.load_path],
+                       "strips": N.SK_LOAD_STRIPS,
+                       "vector": N.SK_LOAD_VECTOR}[self.load_path],
             cells_per_thread=int(self.cells_per_thread),
             fused_iterations=int(self.fused_iterations))
 
@@ -207,7 +210,7 @@ class Stencil:
             raise N.NativeError(rc, "sk_stencil_probe", N.last_error())
         return {"status": N.STATUS_NAMES[rc], "kernel_max": km.value, "tile_bytes": tb.value,
                 "load_path": {N.SK_LOAD_TMA: "tma", N.SK_LOAD_BITPLANE: "bitplane",
-                              N.SK_LOAD_STRIPS: "strips"}.get(
+                              N.SK_LOAD_STRIPS: "strips", N.SK_LOAD_VECTOR: "vector"}.get(
                     lp.value, "explicit")}
 
     def kernel_max(self) -> int:

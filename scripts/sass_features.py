@@ -78,7 +78,7 @@ def main() -> int:
     funcs = sass_functions(OBJ)
 
     def counts_for(op: str) -> dict[str, int]:
-        want = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024(, false)?>\(")
+        want = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024(, false(, 1)?)?>\(")
         hits = [n for n in funcs if want.match(n)]
         if len(hits) != 1:
             raise SystemExit(f"no unique SASS function for {want}: {hits[:3]}")

@@ -31,7 +31,7 @@ def test_categorise_bins_every_opcode_once():
 def test_executor_kernels_have_sass_features():
     funcs = sf.sass_functions(sf.OBJ)
     def one(op):
-        want = re.compile(rf"void sk::k_stencil_tma<sk::{op}, float, 8, 1024(, false)?>\(")
+        want = re.compile(rf"void sk::k_stencil_tma<sk::{op}, float, 8, 1024(, false(, 1)?)?>\(")
         hits = [n for n in funcs if want.match(n)]
         assert len(hits) == 1, op
         return sf.categorise(funcs[hits[0]])
