@@ -187,7 +187,9 @@ int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max);
 /* Timed samples of one pass (the sweep's "run", simoracle.cpp:122-141):
  * `warmup` untimed launches, then `samples` launches each bracketed by a
  * cudaEvent pair on an internal stream; when flush_l2 != 0 a buffer of
- * 2 x l2CacheSize is overwritten before every sample.  ms_out[samples]. */
+ * 2 x l2CacheSize is written and then read back (evicting the pass's data
+ * and leaving clean lines, so no write-back debt lands in the pass) before every
+ * sample.  ms_out[samples]. */
 int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, int64_t width,
                     int64_t height, int64_t pitch, int32_t wc, int32_t wr, int32_t warmup,
                     int32_t samples, int32_t flush_l2, double* ms_out);

@@ -170,24 +170,35 @@ template <typename T>
 __device__ __forceinline__ void fixup_tile(T* tile, const Geom& g, int r0, int c0, T pad,
                                            int tid, int nthreads) {
   // `tile` points at the first logical column (box start + tile_offset).
-  const int total = g.tile_h * g.lw;
+  // The in-range cells form one rectangle [tr_lo, tr_hi] x [tc_lo, tc_hi] of
+  // the tile; only the cells around it are visited: the west / east strips
+  // of the in-range rows, then the out-of-range rows in full.
   const int row_lo = -g.above, row_hi = g.H - 1 + g.below;
-  for (int i = tid; i < total; i += nthreads) {
-    int tr = i / g.lw;
-    int tc = i - tr * g.lw;
-    int gr = r0 - g.N + tr;
-    int gc = c0 - g.Wb + tc;
-    bool in = gr >= row_lo && gr <= row_hi && gc >= 0 && gc < g.W;
-    if (in) continue;
-    T v;
-    if (g.mode == 0) {
-      v = pad;
-    } else {
-      int cr = clampi(gr, row_lo, row_hi) - (r0 - g.N);
-      int cc = clampi(gc, 0, g.W - 1) - (c0 - g.Wb);
+  const int gr0 = r0 - g.N, gc0 = c0 - g.Wb;  // global coords of tile cell (0, 0)
+  const int tr_lo = max(0, row_lo - gr0), tr_hi = min(g.tile_h - 1, row_hi - gr0);
+  const int tc_lo = max(0, -gc0), tc_hi = min(g.lw - 1, g.W - 1 - gc0);
+  const int in_rows = max(0, tr_hi - tr_lo + 1);
+  const int west = tc_lo, side = west + (g.lw - 1 - tc_hi);
+  const int n_side = in_rows * side;
+  const int n_rows = (g.tile_h - in_rows) * g.lw;
+  auto patch = [&](int tr, int tc) {
+    T v = pad;
+    if (g.mode != 0) {
+      const int cr = clampi(tr, tr_lo, tr_hi);
+      const int cc = clampi(tc, tc_lo, tc_hi);
       v = tile[cr * g.tile_w + cc];
     }
     tile[tr * g.tile_w + tc] = v;
+  };
+  for (int i = tid; i < n_side; i += nthreads) {
+    const int q = i / side;
+    const int k = i - q * side;
+    patch(tr_lo + q, k < west ? k : tc_hi + 1 + (k - west));
+  }
+  for (int i = tid; i < n_rows; i += nthreads) {
+    const int q = i / g.lw;
+    const int tc = i - q * g.lw;
+    patch(q < tr_lo ? q : in_rows + q, tc);
   }
 }
 

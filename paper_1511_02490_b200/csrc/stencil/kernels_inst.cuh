@@ -23,7 +23,8 @@ KernelPtr vector_for_k(int K) {
     case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, 1024, false, V>);
     case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, 1024, false, V>);
     case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, 1024, false, V>);
-    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, false, V>);
+    case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, false, V>);
+    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 16, 1024, false, V>);
   }
 }
 

@@ -159,6 +159,11 @@ int validate_desc(const sk_stencil_desc* d) {
         d->cells_per_thread != 32) {
       return fail(SK_EINVAL, "bit-plane cells_per_thread (rows per work-item) must be 0, 8, 16 or 32");
     }
+  } else if (d->load_path == SK_LOAD_VECTOR) {
+    if (d->cells_per_thread != 0 && d->cells_per_thread != 1 && d->cells_per_thread != 2 &&
+        d->cells_per_thread != 4 && d->cells_per_thread != 8 && d->cells_per_thread != 16) {
+      return fail(SK_EINVAL, "vector cells_per_thread (rows per work-item) must be 0 (auto), 1, 2, 4, 8 or 16");
+    }
   } else if (d->cells_per_thread != 0 && d->cells_per_thread != 1 && d->cells_per_thread != 2 &&
       d->cells_per_thread != 4 && d->cells_per_thread != 8) {
     return fail(SK_EINVAL, "cells_per_thread must be 0 (auto), 1, 2, 4 or 8");
@@ -395,20 +400,35 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
                          : kernels_for_desc(d, K);
   if (!kp.tma || !kp.explicit_) return fail(SK_EINVAL, "kernel table has no entry for K=%d", K);
   const bool drv = custom != nullptr;
-  // vector work-items: V = 16 B of cells per work-item row (vector.cuh)
-  const bool vec_path = !drv && d.load_path == SK_LOAD_VECTOR;
-  int V = 1;
-  if (vec_path) {
-    kp.tma = vector_for_desc(d, K);
-    if (!kp.tma) {
-      return fail(SK_ENOTSUP, "no vector kernel for op %d with border (%d,%d,%d,%d)", d.op, d.north,
-                  d.south, d.east, d.west);
-    }
-    V = static_cast<int>(16 / dtype_size(d.dtype));
-  }
   plan->driver_handle = drv;
   // temporal blocking: TB generations per launch (TMA path only)
   const int TB = (!drv && d.fused_iterations > 1) ? d.fused_iterations : 1;
+  // Vector work-items (vector.cuh): V = 16 B of cells per work-item row.
+  // SK_LOAD_VECTOR demands them; AUTO takes them for one-pass launches of
+  // ops that have a vector form whenever the tile fits one TMA box and the
+  // buffers are 16-B aligned (the scalar TMA kernel otherwise).
+  bool vec_path = false;
+  int V = 1;
+  if (!drv && TB == 1 && (d.load_path == SK_LOAD_VECTOR || d.load_path == SK_LOAD_AUTO)) {
+    KernelPtr vk = vector_for_desc(d, K);
+    if (!vk && d.load_path == SK_LOAD_VECTOR) {
+      return fail(SK_ENOTSUP, "no vector kernel for op %d with border (%d,%d,%d,%d)", d.op, d.north,
+                  d.south, d.east, d.west);
+    }
+    if (vk) {
+      const int es_ = static_cast<int>(dtype_size(d.dtype));
+      const int vec_ = 16 / es_;
+      const long long lw_ = static_cast<long long>(wc) * vec_ + d.east + d.west;
+      const long long box_w = (lw_ + ((-d.west) & (vec_ - 1)) + vec_ - 1) / vec_ * vec_;
+      const bool aligned = (pitch_in * es_) % 16 == 0 && (pitch_out * es_) % 16 == 0 &&
+                           (in == nullptr || reinterpret_cast<uintptr_t>(in) % 16 == 0);
+      if (d.load_path == SK_LOAD_VECTOR || (box_w <= 256 && aligned)) {
+        vec_path = true;
+        V = vec_;
+        kp.tma = vk;
+      }
+    }
+  }
   if (TB > 1) {
     kp.tma = fused_for_desc(d, K, TB);
     if (!kp.tma) return fail(SK_ENOTSUP, "no fused (TB=%d) kernel for op %d", TB, d.op);
@@ -479,7 +499,9 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
     if (g.tile_w > 256) {
       return fail(SK_REFUSED, "vector tile %d columns wide exceeds one TMA box (256)", g.tile_w);
     }
-    if (!tma_ok) return fail(SK_ENOTSUP, "the vector path needs 16-B aligned input and pitch");
+    if (!tma_ok || (pitch_out * es) % 16 != 0) {
+      return fail(SK_ENOTSUP, "the vector path needs 16-B aligned input and pitches");
+    }
     use_tma = true;
   }
   const KernelAttr& attr = use_tma ? a_tma : a_exp;
@@ -588,6 +610,15 @@ int launch(const sk_stencil_desc& d, const void* in, void* out, long long W, lon
   if (int rc = make_plan(d, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan, custom)) {
     return rc;
   }
+  if (plan.g.V > 1 && d.load_path == SK_LOAD_AUTO && reinterpret_cast<uintptr_t>(out) % 16 != 0) {
+    // AUTO chose vector work-items, but their 16-B row stores need an
+    // aligned output: take the scalar TMA kernel instead
+    sk_stencil_desc scalar = d;
+    scalar.load_path = SK_LOAD_TMA;
+    if (int rc = make_plan(scalar, W, H, pitch_in, pitch_out, above, below, wc, wr, in, &plan, custom)) {
+      return rc;
+    }
+  }
   long long used_above = plan.g.above;
   long long total_rows = H + plan.g.above + plan.g.below;
   switch (d.dtype) {
@@ -643,7 +674,8 @@ int scratch(Scratch** out) {
       return fail(SK_ECUDA, "stream/event creation failed");
     }
     s.flush_bytes = static_cast<size_t>(info.l2_bytes) * 2;
-    if (cudaMalloc(&s.flush, s.flush_bytes) != cudaSuccess) {
+    if (cudaMalloc(&s.flush, s.flush_bytes) != cudaSuccess ||
+        cudaMemset(s.flush, 0, s.flush_bytes) != cudaSuccess) {
       return fail(SK_ECUDA, "L2 flush buffer allocation failed");
     }
   }
@@ -680,6 +712,22 @@ StreamBits::~StreamBits() {
   for (void* q : p) {
     if (q) cudaFreeAsync(q, stream);
   }
+}
+
+// L2 scrub between timed samples, second half: READ back the 2 x L2 buffer
+// the memset just wrote, so the next pass finds none of its input in L2 and
+// the cache holds clean lines only - the scrub's (and the previous pass's)
+// dirty lines are written back here, not during the next timed pass.  (A
+// memset alone left ~2 x L2 of dirty lines whose write-back was charged to
+// the pass: +6 us on the 32 us config-4 pass.)
+__global__ void k_l2_scrub(const uint4* __restrict__ p, long long n, unsigned* sink) {
+  unsigned acc = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint4 v = p[i];
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u && n < 0) *sink = acc;  // never true: keeps the loads
 }
 
 // Word-wise device comparison; *diff counts differing 16-B words.
@@ -872,7 +920,16 @@ int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, 
     }
   }
   for (int i = 0; i < samples; ++i) {
-    if (flush_l2) cudaMemsetAsync(s->flush, i & 0xff, s->flush_bytes, s->stream);
+    if (flush_l2) {
+      // write 2 x L2 (evicts everything), then read it back (the written
+      // lines leave dirty during this read, not during the timed pass)
+      cudaMemsetAsync(s->flush, i & 0xff, s->flush_bytes, s->stream);
+      DeviceInfo info;
+      if (int rc = current_device_info(&info)) return rc;
+      k_l2_scrub<<<info.sms * 4, 512, 0, s->stream>>>(static_cast<const uint4*>(s->flush),
+                                                     static_cast<long long>(s->flush_bytes / 16),
+                                                     static_cast<unsigned*>(s->flush));
+    }
     cudaEventRecord(s->events[2 * i], s->stream);
     if (int rc = launch(*desc, d_in, d_out, width, height, pitch, pitch, 0, 0, wc, wr, s->stream)) {
       cudaStreamSynchronize(s->stream);

@@ -365,7 +365,9 @@ int sk_stencil_iterate_peer(const sk_stencil_desc* desc, void* d_a, void* d_b, i
     int dev = 0;
     current_device_info(&info, &dev);
     const char* a0 = static_cast<const char*>(d_a) + N * row_bytes;
-    if (m > 0 && make_plan(d, width, rows, pitch, pitch, g.above, g.below, wc, wr, a0, &fplan) == SK_OK &&
+    sk_stencil_desc scalar = d;  // the PEER kernels are scalar work-items
+    if (scalar.load_path == SK_LOAD_AUTO) scalar.load_path = SK_LOAD_TMA;
+    if (m > 0 && make_plan(scalar, width, rows, pitch, pitch, g.above, g.below, wc, wr, a0, &fplan) == SK_OK &&
         fplan.tma && !fplan.driver_handle && fplan.g.tile_rows >= m) {
       KernelPtr k = peer_tma_kernel(d, fplan.g.K);
       KernelAttr ka;

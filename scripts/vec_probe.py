@@ -12,6 +12,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1511_02490_b200 import RefusedParameter, IllegalWorkgroupSize, Stencil  # noqa: E402
+from paper_1511_02490_b200._native import NativeError  # noqa: E402
 
 PEAK = 6448.7
 try:
@@ -39,7 +40,7 @@ for name in names:
         for wc, wr in SIZES:
             try:
                 ms = st.time(a, b, wc, wr, samples=10, warmup=2, flush_l2=True)
-            except (RefusedParameter, IllegalWorkgroupSize):
+            except (RefusedParameter, IllegalWorkgroupSize, NativeError):
                 continue
             res.append((sum(ms) / len(ms), wc, wr))
         res.sort()

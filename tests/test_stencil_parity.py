@@ -206,10 +206,16 @@ def test_kernel_max_and_probe_fields():
     st = Stencil(op="five_point", dtype="float32", cells_per_thread=1)
     km = st.kernel_max()
     assert 64 <= km <= 1024
+    # AUTO takes 16-B vector work-items (4 fp32 cells per row) when the tile fits one TMA box
     p = st.probe(1024, 1024, 32, 8)
-    assert p["status"] == "OK" and p["load_path"] == "tma"
-    assert p["tile_bytes"] == (32 + 2) * (8 + 2) * 4
-    p4 = Stencil(op="five_point", dtype="float32", cells_per_thread=4).probe(1024, 1024, 32, 8)
+    assert p["status"] == "OK" and p["load_path"] == "vector"
+    assert p["tile_bytes"] == (4 * 32 + 2) * (8 + 2) * 4
+    # ... and the scalar TMA kernel past 256 box columns (4 * 64 + 2)
+    assert st.probe(1024, 1024, 64, 8)["load_path"] == "tma"
+    ps = Stencil(op="five_point", dtype="float32", cells_per_thread=1, load_path="tma").probe(1024, 1024, 32, 8)
+    assert ps["load_path"] == "tma" and ps["tile_bytes"] == (32 + 2) * (8 + 2) * 4
+    p4 = Stencil(op="five_point", dtype="float32", cells_per_thread=4,
+                 load_path="tma").probe(1024, 1024, 32, 8)
     assert p4["tile_bytes"] == (32 + 2) * (8 * 4 + 2) * 4
 
 

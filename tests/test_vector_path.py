@@ -112,8 +112,21 @@ def test_vector_contract():
         Stencil(op="heat", dtype="float32", load_path="vector", fused_iterations=2)(
             x, torch.empty_like(x), 32, 2)
     assert e.value.code == N.SK_ENOTSUP
-    # misaligned output rows
+    # misaligned output pitch: not a vector-path buffer
     y = torch.zeros((256, 1025), device="cuda")
     with pytest.raises(N.NativeError) as e:
         st(x, y[:, 1:], 32, 2)
+    assert e.value.code == N.SK_ENOTSUP
+    # aligned pitch, output base 4 B off: the 16-B row stores are rejected ...
+    flat = torch.zeros(256 * 1024 + 4, device="cuda")
+    y = flat[1:1 + 256 * 1024].view(256, 1024)
+    with pytest.raises(N.NativeError) as e:
+        st(x, y, 32, 2)
     assert e.value.code == N.SK_EINVAL
+    # ... while AUTO falls back to the scalar TMA kernel for that output
+    x.uniform_()
+    Stencil(op="heat", dtype="float32")(x, y, 32, 2)
+    want = torch.empty_like(x)
+    Stencil(op="heat", dtype="float32", load_path="tma")(x, want, 32, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
