@@ -36,7 +36,7 @@ struct SweepConfig {
   int warmup = 3;            // untimed launches before the samples
   bool flush_l2 = true;      // overwrite 2 x L2 before every sample
   int max_wgsize_cap = 0;    // optional cap on the effective maximum (0 = none)
-  bool validate = true;      // every size's output must equal the gold standard
+  bool validate = true;      // every size's output must equal the gold standard (else rejected)
   std::uint64_t seed = 1;    // input grid seed (reference Rng stream)
   int border_mode = SK_BORDER_NEAREST;
   double pad_value = 0.0;
@@ -60,6 +60,9 @@ struct CollectResult {
   SampleTable table;
   RefusedRecord refused;
   ContextRecord contexts;
+  // sizes whose output differed from the gold standard (an explicit-load
+  // pass): rejected before timing, also listed as refused; must be empty
+  std::map<std::string, std::set<WorkgroupSize>> rejected;
   std::map<std::string, std::size_t> gold_mismatches;  // per scenario, must be 0
 };
 

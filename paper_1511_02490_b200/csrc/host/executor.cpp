@@ -147,6 +147,19 @@ std::vector<double> run(const Scenario& s, WorkgroupSize w, const SweepConfig& c
   return timed_samples(d, s, g, w, cfg);
 }
 
+// The gold standard of a scenario: one pass through the explicit-load
+// kernel (one column per work-item, K = 1, 32x8 block) - an independent code
+// path from the TMA / vector kernels whose sizes are being timed.
+void gold_output(const sk_stencil_desc& d, const Scenario& s, const Grids& g, void* gold) {
+  sk_stencil_desc e = d;
+  e.load_path = SK_LOAD_EXPLICIT;
+  e.cells_per_thread = 1;
+  const int rc = sk_stencil_launch(&e, g.in, gold, s.dataset.width, s.dataset.height, s.dataset.width,
+                                   s.dataset.width, 0, 0, 32, 8, nullptr);
+  if (rc != SK_OK) device_fail("gold-standard pass (" + s.id + ")");
+  check_cuda(cudaDeviceSynchronize(), "gold-standard pass");
+}
+
 CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig& cfg,
                       const ProgressFn& progress) {
   if (scenarios.empty()) throw InvalidArgument("collect requires at least one scenario");
@@ -156,8 +169,13 @@ CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig&
     Grids g(s, cfg);
     const auto space = enumerate_space(effective_max(s, cfg));
     std::set<WorkgroupSize>& refused = res.refused[s.id];
-    void* gold = nullptr;  // output of the first measured size = the gold standard
-    std::size_t mismatches = 0, done = 0;
+    std::set<WorkgroupSize>& rejected = res.rejected[s.id];
+    void* gold = nullptr;
+    if (cfg.validate) {
+      check_cuda(cudaMalloc(&gold, g.bytes), "cudaMalloc(gold)");
+      gold_output(d, s, g, gold);
+    }
+    std::size_t done = 0;
     for (const WorkgroupSize& w : space) {
       const int rc = sk_stencil_probe(&d, s.dataset.width, s.dataset.height, w.cols(), w.rows(), nullptr,
                                       nullptr, nullptr);
@@ -166,32 +184,40 @@ CollectResult collect(const std::vector<Scenario>& scenarios, const SweepConfig&
       } else if (rc != SK_OK) {
         device_fail("sk_stencil_probe(" + s.id + ", " + w.str() + ")");
       } else {
-        try {
-          res.table.add_row(s.id, w, timed_samples(d, s, g, w, cfg));
-        } catch (const RefusedParameter&) {
-          refused.insert(w);  // launch-time refusal (non-sticky)
-          continue;
-        }
+        // validate before timing: a size whose output differs from the gold
+        // standard is rejected (recorded, never timed)
+        bool ok = true;
         if (cfg.validate) {
-          if (!gold) {
-            check_cuda(cudaMalloc(&gold, g.bytes), "cudaMalloc(gold)");
-            check_cuda(cudaMemcpy(gold, g.out, g.bytes, cudaMemcpyDeviceToDevice), "cudaMemcpy(gold)");
-          } else {
-            int32_t equal = 0;
-            if (sk_buffers_equal(gold, g.out, static_cast<int64_t>(g.bytes), &equal) != SK_OK) {
-              device_fail("sk_buffers_equal");
-            }
-            if (!equal) {
-              ++mismatches;
-              std::fprintf(stderr, "GOLD MISMATCH %s %s\n", s.id.c_str(), w.str().c_str());
-            }
+          const int lrc = sk_stencil_launch(&d, g.in, g.out, s.dataset.width, s.dataset.height,
+                                            s.dataset.width, s.dataset.width, 0, 0, w.cols(), w.rows(), nullptr);
+          if (lrc == SK_REFUSED) {
+            refused.insert(w);
+            if (progress) progress(s, ++done, space.size());
+            continue;
+          }
+          if (lrc != SK_OK) device_fail("validation pass (" + s.id + ", " + w.str() + ")");
+          int32_t equal = 0;
+          if (sk_buffers_equal(gold, g.out, static_cast<int64_t>(g.bytes), &equal) != SK_OK) {
+            device_fail("sk_buffers_equal");
+          }
+          ok = equal != 0;
+        }
+        if (!ok) {
+          rejected.insert(w);
+          refused.insert(w);  // unusable: the evaluation treats it like a refusal
+          std::fprintf(stderr, "GOLD MISMATCH %s %s (rejected, not timed)\n", s.id.c_str(), w.str().c_str());
+        } else {
+          try {
+            res.table.add_row(s.id, w, timed_samples(d, s, g, w, cfg));
+          } catch (const RefusedParameter&) {
+            refused.insert(w);  // launch-time refusal (non-sticky)
           }
         }
       }
       if (progress) progress(s, ++done, space.size());
     }
     cudaFree(gold);
-    res.gold_mismatches[s.id] = mismatches;
+    res.gold_mismatches[s.id] = rejected.size();
     res.contexts.emplace(s.id, scenario_context(s, cfg, refused));
   }
   return res;
