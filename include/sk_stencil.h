@@ -170,6 +170,28 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
                        int64_t height, int64_t pitch, int32_t iterations, int32_t wc,
                        int32_t wr, void* stream, int32_t* result_in_b);
 
+/* Row-sharded iterated stencil with the per-generation halo exchange over
+ * NCCL (the "sk_halo_step(..., ncclComm_t)" of §8b).  This
+ * rank owns `rows` rows of the global grid; d_a / d_b point at the first of
+ * N halo rows above them and hold N + rows + S rows of `pitch` elements.
+ * Per generation: ncclGroupStart; send the first S owned rows to rank-1 and
+ * receive N halo rows from it; send the last N owned rows to rank+1 and
+ * receive S halo rows from it; ncclGroupEnd - on an internal exchange
+ * stream, while the interior rows [N, rows-S) compute on `stream`; then the
+ * two boundary strips.  Rank 0's north and rank nranks-1's south halos are
+ * border cells (pad / nearest), so the ranks together compute exactly the
+ * single-GPU result.  `comm` is an ncclComm_t of the NCCL loaded in the
+ * process (resolved at run time; the library does not link NCCL), with
+ * this process's `rank` of `nranks`; unused when nranks == 1.  One
+ * generation per launch: fused_iterations <= 1, one-pass load paths
+ * (SK_ENOTSUP otherwise).  *result_in_b as in sk_stencil_iterate.  The
+ * single-GPU replacement for the reference's simulated run (simoracle.cpp:
+ * 122-141) applied to an iterated multi-GPU step. */
+int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_t width,
+                            int64_t rows, int64_t pitch, int32_t iterations, int32_t wc, int32_t wr,
+                            void* comm, int32_t rank, int32_t nranks, void* stream,
+                            int32_t* result_in_b);
+
 /* Zero-work legality probe for (wc, wr) on the current device.  Returns
  * SK_OK (legal), SK_OVERSIZED or SK_REFUSED.  Optional outputs: the
  * per-kernel maximum block size (cudaFuncAttributes.maxThreadsPerBlock,

@@ -129,6 +129,8 @@ _PROTOTYPES = {
     "sk_ipc_export": (_i32, [_vp, ctypes.POINTER(sk_ipc_handle)]),
     "sk_ipc_import": (_i32, [ctypes.POINTER(sk_ipc_handle), ctypes.POINTER(_vp)]),
     "sk_ipc_close": (_i32, [_vp]),
+    "sk_stencil_iterate_nccl": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp,
+                                       _i32, _i32, _vp, ctypes.POINTER(ctypes.c_int32)]),
     "sk_stencil_iterate_peer": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32,
                                        ctypes.POINTER(sk_halo_peers), _vp, ctypes.POINTER(_i64),
                                        _vp, ctypes.POINTER(_i32)]),

@@ -333,6 +333,36 @@ def connect_peers(a: torch.Tensor, b: torch.Tensor, control: torch.Tensor, shard
     return links
 
 
+def nccl_comm_ptr(group=None) -> int:
+    """The raw ncclComm_t of torch's NCCL process group (for the C-ABI)."""
+    pg = group or dist.distributed_c10d._get_default_group()
+    return int(pg._get_backend(torch.device("cuda"))._comm_ptr())
+
+
+def iterate_sharded_nccl(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iterations: int,
+                         stencil, wc: int, wr: int, comm: int | None = None, stream=None) -> torch.Tensor:
+    """`iterations` generations through the C-ABI NCCL schedule
+    (sk_stencil_iterate_nccl): ncclSend/ncclRecv of the halo rows on the
+    library's exchange stream behind the interior pass, then the boundary
+    strips.  `a` / `b` are the shard's N + rows + S row buffers; `comm` is a
+    raw ncclComm_t (default: torch's NCCL group).  Returns the buffer holding
+    the result; bit-identical to iterate_sharded."""
+    from . import _native as N
+
+    shard.check()
+    _one_generation_per_launch(stencil)
+    if shard.world > 1 and comm is None:
+        comm = nccl_comm_ptr()
+    s = (stream or torch.cuda.current_stream(a.device)).cuda_stream
+    in_b = ctypes.c_int32(0)
+    rc = N.lib().sk_stencil_iterate_nccl(ctypes.byref(stencil.desc), a.data_ptr(), b.data_ptr(), shard.width,
+                                         shard.rows, a.stride(0), iterations, wc, wr, comm or None,
+                                         shard.rank, shard.world, s or None, ctypes.byref(in_b))
+    if rc:
+        raise N.NativeError(rc, "sk_stencil_iterate_nccl", N.last_error())
+    return b if in_b.value else a
+
+
 def iterate_sharded_peer(a: torch.Tensor, b: torch.Tensor, shard: RowShard, iterations: int,
                          stencil, wc: int, wr: int, links: PeerLinks, stream=None) -> torch.Tensor:
     """`iterations` generations with the halo exchange fused into the
