@@ -21,6 +21,7 @@
 
 #include "sk_stencil.h"
 #include "wgtb/common.hpp"
+#include "wgtb_c.h"
 
 namespace wgtb {
 
@@ -143,6 +144,40 @@ class Stencil {
   }
 
   const sk_stencil_desc& desc() const { return desc_; }
+
+  // Online-tuned launches (wgtb_c.h, libwgtb): the trained model picks the
+  // workgroup size per (grid, device) and re-picks when a launch is refused.
+  //   auto tuned = heat.autotuned("results/b200/model.json", "he.json");
+  //   tuned(d_in, d_out, W, H);   // tuned.wc(), tuned.wr(): the size that ran
+  class Tuned {
+   public:
+    Tuned(const Stencil& s, std::string model_json, std::string kernel_json)
+        : desc_(s.desc_), model_(std::move(model_json)), kernel_(std::move(kernel_json)) {}
+    void operator()(const T* d_in, T* d_out, int64_t W, int64_t H, void* stream = nullptr, int64_t pitch = 0) {
+      const int64_t p = pitch ? pitch : W;
+      if (wgtb_launch_tuned(model_.c_str(), kernel_.c_str(), &desc_, d_in, d_out, W, H, p, p, stream, &wc_, &wr_,
+                            &proposals_) != 0) {
+        throw NoLegalParameter(std::string("Stencil::Tuned: ") + wgtb_last_error());
+      }
+    }
+    // external refusal feedback for the W x H session
+    void refuse(int64_t W, int64_t H, int wc, int wr) {
+      if (wgtb_tuned_refuse(model_.c_str(), kernel_.c_str(), &desc_, W, H, wc, wr) != 0) {
+        throw InvalidArgument(std::string("Stencil::Tuned::refuse: ") + wgtb_last_error());
+      }
+    }
+    int wc() const { return wc_; }
+    int wr() const { return wr_; }
+    int proposals() const { return proposals_; }
+
+   private:
+    sk_stencil_desc desc_;
+    std::string model_, kernel_;
+    int32_t wc_ = 0, wr_ = 0, proposals_ = 0;
+  };
+  Tuned autotuned(std::string model_json, std::string kernel_json) const {
+    return Tuned(*this, std::move(model_json), std::move(kernel_json));
+  }
 
  private:
   sk_stencil_desc desc_{};

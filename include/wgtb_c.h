@@ -26,6 +26,28 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
                  int64_t width, int64_t height, int32_t* wc, int32_t* wr, int32_t* probes,
                  double* elapsed_ms);
 
+/* Online tuning (the paper's runtime loop; the reference
+ * daemon's session, serve.cpp:123-164): one stencil pass with the size the
+ * model proposes for (desc, W, H, current device).  The proposal is cached
+ * per session; when the launch is refused (SK_REFUSED / SK_OVERSIZED) the
+ * size joins the session's refused set and the model re-proposes - Algorithm
+ * 1's fallbacks or Algorithm 2's next candidate - until a launch runs (at
+ * most 64 proposals).  *wc_used / *wr_used: the size that ran; *proposals:
+ * proposals made in this session so far.  0, or -1 with wgtb_last_error(). */
+int wgtb_launch_tuned(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                      const void* d_in, void* d_out, int64_t width, int64_t height, int64_t pitch_in,
+                      int64_t pitch_out, void* stream, int32_t* wc_used, int32_t* wr_used,
+                      int32_t* proposals);
+
+/* External refusal feedback for a session (serve.cpp's {"type":"refused"}):
+ * the size is never proposed again for it; the next wgtb_launch_tuned
+ * re-proposes if it was the current proposal. */
+int wgtb_tuned_refuse(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                      int64_t width, int64_t height, int32_t wc, int32_t wr);
+
+/* Forget every session. */
+void wgtb_tuned_reset(void);
+
 const char* wgtb_last_error(void);
 
 #ifdef __cplusplus

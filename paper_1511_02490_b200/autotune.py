@@ -25,6 +25,17 @@ def lib():
                                    ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_double)]
+        h.wgtb_launch_tuned.restype = ctypes.c_int
+        h.wgtb_launch_tuned.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(N.sk_stencil_desc),
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(ctypes.c_int32)]
+        h.wgtb_tuned_refuse.restype = ctypes.c_int
+        h.wgtb_tuned_refuse.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(N.sk_stencil_desc),
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+        h.wgtb_tuned_reset.restype = None
+        h.wgtb_tuned_reset.argtypes = []
         h.wgtb_last_error.restype = ctypes.c_char_p
         _lib = h
     return _lib
@@ -40,3 +51,42 @@ def predict(stencil, width: int, height: int, kernel_json: str | Path,
     if rc != 0:
         raise RuntimeError(f"wgtb_predict: {lib().wgtb_last_error().decode()}")
     return {"wc": wc.value, "wr": wr.value, "probes": probes.value, "ms": ms.value}
+
+
+class Tuned:
+    """Online-tuned launches of `stencil` (wgtb_launch_tuned): the model
+    proposes the workgroup size once per (grid, device) session and
+    re-proposes when a launch is refused - the refused size is never proposed
+    again in the session (reference serve.cpp:123-164)."""
+
+    def __init__(self, stencil, kernel_json: str | Path, model_json: str | Path = RESULTS / "model.json"):
+        self.stencil = stencil
+        self.kernel_json = str(kernel_json).encode()
+        self.model_json = str(model_json).encode()
+        self.last = None  # (wc, wr, proposals) of the last launch
+
+    def __call__(self, inp, out, stream=None) -> tuple[int, int]:
+        import torch
+
+        self.stencil._check_device(inp, out)
+        h, w = out.shape
+        s = (stream or torch.cuda.current_stream(inp.device)).cuda_stream
+        wc, wr, props = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        rc = lib().wgtb_launch_tuned(self.model_json, self.kernel_json, ctypes.byref(self.stencil.desc),
+                                     inp.data_ptr(), out.data_ptr(), w, h, inp.stride(0), out.stride(0),
+                                     s or None, ctypes.byref(wc), ctypes.byref(wr), ctypes.byref(props))
+        if rc != 0:
+            raise RuntimeError(f"wgtb_launch_tuned: {lib().wgtb_last_error().decode()}")
+        self.last = (wc.value, wr.value, props.value)
+        return wc.value, wr.value
+
+    def refuse(self, width: int, height: int, wc: int, wr: int) -> None:
+        """External refusal feedback for the (width x height) session."""
+        rc = lib().wgtb_tuned_refuse(self.model_json, self.kernel_json, ctypes.byref(self.stencil.desc),
+                                     width, height, wc, wr)
+        if rc != 0:
+            raise RuntimeError(f"wgtb_tuned_refuse: {lib().wgtb_last_error().decode()}")
+
+    @staticmethod
+    def reset() -> None:
+        lib().wgtb_tuned_reset()

@@ -49,6 +49,116 @@ wgtb::ElementType element_of(int dtype) {
 
 }  // namespace
 
+namespace {
+
+// The session's known-refused sizes under the effective maximum, plus the
+// bundle's prior refusals.
+wgtb::ConstraintContext session_context(const Bundle& b, int dev_max, int kmax,
+                                        const std::set<wgtb::WorkgroupSize>& refused) {
+  std::set<wgtb::WorkgroupSize> known;
+  const int eff = std::min(kmax, dev_max);
+  for (const auto& w : b.prior_refused) {
+    if (w.area() <= eff) known.insert(w);
+  }
+  for (const auto& w : refused) {
+    if (w.area() <= eff) known.insert(w);
+  }
+  return wgtb::ConstraintContext(dev_max, kmax, known);
+}
+
+// Algorithm 1 or 2 (whichever the bundle holds) against `probe`.
+wgtb::WorkgroupSize choose(const Bundle& b, const wgtb::Scenario& s, const wgtb::FeatureVector& f,
+                           const wgtb::ConstraintContext& ctx, const wgtb::ProbeFn& probe) {
+  if (b.regressor) {
+    const auto fm = b.regressor->mode() == wgtb::RegressionMode::Runtime ? wgtb::FitnessMode::RuntimeReciprocal
+                                                                         : wgtb::FitnessMode::Speedup;
+    return wgtb::tune_regress(*b.regressor, f, ctx, fm, probe).w;
+  }
+  const auto strategy = b.fallback == "random" ? wgtb::FallbackStrategy::random(wgtb::fnv1a64(s.id, 0))
+                                               : wgtb::FallbackStrategy::nearest_neighbour();
+  return wgtb::tune_classify(*b.classifier, f, ctx, strategy, probe).w;
+}
+
+// One tuning context on the current device: the inputs of the prediction
+// and what this session has learnt about legality.
+struct Scene {
+  std::shared_ptr<Bundle> bundle;
+  wgtb::Scenario scenario;
+  wgtb::FeatureVector features;
+  int kmax = 0;
+};
+
+Scene make_scene(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc, int64_t width,
+                 int64_t height) {
+  if (!model_json || !kernel_json || !desc) throw wgtb::InvalidArgument("null argument");
+  Scene sc;
+  sc.bundle = load_bundle(model_json);
+  const wgtb::KernelDescriptor k = wgtb::kernel_from_json(nlohmann::json::parse(wgtb::read_text(kernel_json)));
+  wgtb::DatasetDescriptor ds{static_cast<int>(width), static_cast<int>(height), element_of(desc->dtype),
+                             element_of(desc->dtype)};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw wgtb::DeviceError("cudaGetDevice failed");
+  sc.scenario = wgtb::make_scenario(wgtb::device_from_cuda(dev), k, ds);
+  sc.features = wgtb::extract(sc.scenario);
+  if (sk_kernel_max_wgsize(desc, &sc.kmax) != SK_OK) throw wgtb::DeviceError(sk_last_error());
+  return sc;
+}
+
+// Online tuning sessions (the in-process form of serve.cpp's Session),
+// keyed by (model, kernel, descriptor, W, H, device).
+struct Session {
+  Scene scene;
+  std::set<wgtb::WorkgroupSize> refused;  // learnt from launches / callers
+  wgtb::WorkgroupSize w;
+  bool proposed = false;
+  int proposals = 0;
+};
+std::mutex g_sess_mu;
+std::map<std::string, Session> g_sessions;
+
+std::string session_key(const char* model_json, const char* kernel_json, const sk_stencil_desc* d, int64_t width,
+                        int64_t height) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::string key = std::string(model_json) + '\n' + kernel_json + '\n';
+  key.append(reinterpret_cast<const char*>(d), sizeof *d);
+  key += '\n' + std::to_string(width) + 'x' + std::to_string(height) + '@' + std::to_string(dev);
+  return key;
+}
+
+Session& session_for(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc, int64_t width,
+                     int64_t height) {
+  const std::string key = session_key(model_json, kernel_json, desc, width, height);
+  auto it = g_sessions.find(key);
+  if (it == g_sessions.end()) {
+    Session s;
+    s.scene = make_scene(model_json, kernel_json, desc, width, height);
+    it = g_sessions.emplace(key, std::move(s)).first;
+  }
+  return it->second;
+}
+
+// A new proposal: the live device probe, except that sizes this session has
+// seen refused stay refused (serve.cpp:59-61, 150-157).
+void propose(Session& s, const sk_stencil_desc* desc, int64_t width, int64_t height) {
+  const Bundle& b = *s.scene.bundle;
+  const int dev_max = s.scene.scenario.device.device_max_wgsize;
+  const auto ctx = session_context(b, dev_max, s.scene.kmax, s.refused);
+  const wgtb::ProbeFn probe = [&](wgtb::WorkgroupSize w) {
+    if (s.refused.count(w)) return wgtb::ProbeResult::Refused;
+    const int rc = sk_stencil_probe(desc, width, height, w.cols(), w.rows(), nullptr, nullptr, nullptr);
+    if (rc == SK_OK) return wgtb::ProbeResult::Legal;
+    if (rc == SK_OVERSIZED) return wgtb::ProbeResult::Oversized;
+    if (rc == SK_REFUSED) return wgtb::ProbeResult::Refused;
+    throw wgtb::DeviceError(sk_last_error());
+  };
+  s.w = choose(b, s.scene.scenario, s.scene.features, ctx, probe);
+  s.proposed = true;
+  ++s.proposals;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* wgtb_last_error(void) { return g_error.c_str(); }
@@ -58,23 +168,9 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
                  double* elapsed_ms) {
   g_error.clear();
   try {
-    if (!model_json || !kernel_json || !desc || !wc || !wr) throw wgtb::InvalidArgument("null argument");
-    auto bundle = load_bundle(model_json);
-    const wgtb::KernelDescriptor k = wgtb::kernel_from_json(nlohmann::json::parse(wgtb::read_text(kernel_json)));
-    wgtb::DatasetDescriptor ds{static_cast<int>(width), static_cast<int>(height), element_of(desc->dtype),
-                               element_of(desc->dtype)};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) throw wgtb::DeviceError("cudaGetDevice failed");
-    const wgtb::Scenario s = wgtb::make_scenario(wgtb::device_from_cuda(dev), k, ds);
-    const wgtb::FeatureVector f = wgtb::extract(s);
-    int32_t kmax = 0;
-    if (sk_kernel_max_wgsize(desc, &kmax) != SK_OK) throw wgtb::DeviceError(sk_last_error());
-    std::set<wgtb::WorkgroupSize> known;
-    const int eff = std::min<int>(kmax, s.device.device_max_wgsize);
-    for (auto w : bundle->prior_refused) {
-      if (w.area() <= eff) known.insert(w);
-    }
-    const wgtb::ConstraintContext ctx(s.device.device_max_wgsize, kmax, known);
+    if (!wc || !wr) throw wgtb::InvalidArgument("null argument");
+    const Scene sc = make_scene(model_json, kernel_json, desc, width, height);
+    const auto ctx = session_context(*sc.bundle, sc.scenario.device.device_max_wgsize, sc.kmax, {});
     int n_probes = 0;
     const wgtb::ProbeFn probe = [&](wgtb::WorkgroupSize w) {
       ++n_probes;
@@ -85,16 +181,7 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
       throw wgtb::DeviceError(sk_last_error());
     };
     const auto t0 = std::chrono::steady_clock::now();
-    wgtb::WorkgroupSize w;
-    if (bundle->regressor) {
-      const auto fm = bundle->regressor->mode() == wgtb::RegressionMode::Runtime ? wgtb::FitnessMode::RuntimeReciprocal
-                                                                                 : wgtb::FitnessMode::Speedup;
-      w = wgtb::tune_regress(*bundle->regressor, f, ctx, fm, probe).w;
-    } else {
-      const auto strategy = bundle->fallback == "random" ? wgtb::FallbackStrategy::random(wgtb::fnv1a64(s.id, 0))
-                                                         : wgtb::FallbackStrategy::nearest_neighbour();
-      w = wgtb::tune_classify(*bundle->classifier, f, ctx, strategy, probe).w;
-    }
+    const wgtb::WorkgroupSize w = choose(*sc.bundle, sc.scenario, sc.features, ctx, probe);
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     *wc = w.cols();
     *wr = w.rows();
@@ -105,6 +192,57 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
     g_error = e.what();
     return -1;
   }
+}
+
+int wgtb_launch_tuned(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                      const void* d_in, void* d_out, int64_t width, int64_t height, int64_t pitch_in,
+                      int64_t pitch_out, void* stream, int32_t* wc_used, int32_t* wr_used,
+                      int32_t* proposals) {
+  g_error.clear();
+  try {
+    std::lock_guard<std::mutex> lk(g_sess_mu);
+    Session& s = session_for(model_json, kernel_json, desc, width, height);
+    for (int attempt = 0; attempt < 64; ++attempt) {
+      if (!s.proposed) propose(s, desc, width, height);
+      const int rc = sk_stencil_launch(desc, d_in, d_out, width, height, pitch_in, pitch_out, 0, 0, s.w.cols(),
+                                       s.w.rows(), stream);
+      if (rc == SK_OK) {
+        if (wc_used) *wc_used = s.w.cols();
+        if (wr_used) *wr_used = s.w.rows();
+        if (proposals) *proposals = s.proposals;
+        return 0;
+      }
+      if (rc != SK_REFUSED && rc != SK_OVERSIZED) throw wgtb::DeviceError(sk_last_error());
+      // refusal feedback: never propose this size again in this session
+      s.refused.insert(s.w);
+      s.proposed = false;
+    }
+    throw wgtb::NoLegalParameter("64 proposals in a row were refused at launch");
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1;
+  }
+}
+
+int wgtb_tuned_refuse(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                      int64_t width, int64_t height, int32_t wc, int32_t wr) {
+  g_error.clear();
+  try {
+    std::lock_guard<std::mutex> lk(g_sess_mu);
+    Session& s = session_for(model_json, kernel_json, desc, width, height);
+    const wgtb::WorkgroupSize w(wc, wr);
+    s.refused.insert(w);
+    if (s.proposed && s.w == w) s.proposed = false;
+    return 0;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1;
+  }
+}
+
+void wgtb_tuned_reset(void) {
+  std::lock_guard<std::mutex> lk(g_sess_mu);
+  g_sessions.clear();
 }
 
 }  // extern "C"
