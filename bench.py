@@ -60,7 +60,16 @@ def workload_config(config: str, world: int, scaling: str) -> dict:
     }
 
 
-KERNEL_NAMES = {"gol": "k_stencil_tma<Gol,int>", "heat": "k_stencil_tma<Heat,float>"}
+KERNEL_NAMES = {"gol": "Gol, int", "heat": "Heat, float"}
+
+
+def kernel_label(st, config, W, H, wc, wr):
+    """The one-pass kernel a launch at (wc, wr) takes (probe's load path)."""
+    lp = st.probe(W, H, wc, wr)["load_path"]
+    k = KERNEL_NAMES[config]
+    if lp == "vector":
+        return f"k_stencil_tma<{k}, K, 1024, false, V=4> (16-B vector work-items)"
+    return f"k_stencil_tma<{k}, K, 1024> ({lp})"
 
 
 def measured_hbm_peak():
@@ -328,9 +337,18 @@ def run_ours(args):
             links = None
             transport = "nccl (peer mapping unavailable" + (f": {why})" if not ok else ")")
 
+    nccl_abi = world > 1 and links is None and args.backend == "nccl" and not args.no_overlap
+    if nccl_abi:
+        from paper_1511_02490_b200.distributed import iterate_sharded_nccl, nccl_comm_ptr
+
+        comm = nccl_comm_ptr()
+        transport = "nccl (C-ABI sk_stencil_iterate_nccl: send/recv behind the interior pass)"
+
     def one_step():
         if links is not None:
             return iterate_sharded_peer(a, b, shard, iters, st, wc, wr, links)
+        if nccl_abi:
+            return iterate_sharded_nccl(a, b, shard, iters, st, wc, wr, comm=comm)
         if world > 1 and not args.no_overlap:
             return iterate_sharded_overlapped(a, b, shard, iters, st, wc, wr)
         return iterate_sharded(a, b, shard, iters, step_fn)
@@ -435,7 +453,7 @@ def run_ours(args):
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_gen,
                          "avg_launch_us": round(per_gen_s * 1e6, 2),
-                         "kernel": KERNEL_NAMES[args.config],
+                         "kernel": kernel_label(st, args.config, W, shard.rows, wc, wr),
                          "note": "per rank, per generation (one launch at N=1)"},
             "cpu_baseline": cpu,
             "temporal_blocking": temporal,

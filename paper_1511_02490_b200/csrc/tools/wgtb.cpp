@@ -96,9 +96,32 @@ std::vector<Scenario> filtered(const DescriptorSet& set, const Args& a) {
 
 EvalData load_eval(const Args& a) {
   auto scenarios = filtered(load_descriptors(a.need("--scenarios")), a);
-  SampleTable table = load_samples(a.need("--samples"));
-  RefusedRecord refused = a.has("--refused") ? load_refused(a.get("--refused")) : RefusedRecord{};
-  ContextRecord contexts = load_contexts(a.need("--contexts"), refused);
+  // --samples / --refused / --contexts may repeat: the files are layered in
+  // order, a later file replacing whole scenarios of the earlier ones (e.g.
+  // the round-1 study + the 30-observation re-sweep of the real kernels)
+  a.need("--samples");
+  a.need("--contexts");
+  SampleTable table;
+  for (const auto& f : a.all("--samples")) {
+    SampleTable layer = load_samples(f);
+    for (const auto& id : layer.scenario_ids()) {
+      table.erase_scenario(id);
+      for (const auto& [w, runs] : layer.scenario_rows(id)) table.add_row(id, w, runs);
+    }
+  }
+  // the i-th --refused file belongs to the i-th --contexts file
+  const auto ctx_files = a.all("--contexts"), ref_files = a.all("--refused");
+  if (!ref_files.empty() && ref_files.size() != ctx_files.size()) {
+    throw UsageError("give one --refused per --contexts (or none)");
+  }
+  ContextRecord contexts;
+  for (std::size_t i = 0; i < ctx_files.size(); ++i) {
+    const RefusedRecord refused = ref_files.empty() ? RefusedRecord{} : load_refused(ref_files[i]);
+    for (auto& [id, ctx] : load_contexts(ctx_files[i], refused)) {
+      contexts.erase(id);
+      contexts.emplace(id, std::move(ctx));
+    }
+  }
   std::vector<Scenario> with_data;
   for (auto& s : scenarios) {
     if (table.has_scenario(s.id) && contexts.contains(s.id)) with_data.push_back(std::move(s));
