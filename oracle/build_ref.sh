@@ -45,3 +45,22 @@ if [ -f "$LIBDIR/libwgtb.so" ] && { [ ! -f "$HARNESS" ] || [ "$REPO/tests/parity
     -Wl,-rpath,"$LIBDIR" -Wl,-rpath,/usr/local/cuda/lib64
 fi
 echo "$HARNESS"
+
+# The reference-side B200 binding (integration/b200_backend.cpp, INTEGRATION.md
+# §2) linked into the reference's own collect(): simoracle.cpp is compiled
+# without inlining and its run / kernel_max_wgsize / is_refused are weakened,
+# so the binding's strong definitions replace the simulator while collect()
+# and scenario_context() remain the reference's code.
+BIN2="$OUT/b200_collect"
+if [ -f "$LIBDIR/libsk_stencil.so" ] && { [ ! -f "$BIN2" ] || [ "$REPO/integration/b200_backend.cpp" -nt "$BIN2" ] || [ "$REPO/tests/parity/b200_collect_main.cpp" -nt "$BIN2" ] || [ "$LIBDIR/libsk_stencil.so" -nt "$BIN2" ]; }; then
+  $CXX -std=c++20 -O0 -fno-inline -fPIC -I"$REF/include" -I"$JSON_INC" -c "$REF/src/simoracle.cpp" -o "$OUT/obj_simoracle_weak.o"
+  syms=$(nm "$OUT/obj_simoracle_weak.o" | awk '$2=="T"{print $3}' | grep -E '^_ZN6wgtune(3run|17kernel_max_wgsize|10is_refused)E')
+  args=""; for s in $syms; do args="$args --weaken-symbol=$s"; done
+  objcopy $args "$OUT/obj_simoracle_weak.o"
+  others=""; for s in space scenario features synthgen datastore learn tuner bench; do others="$others $OUT/obj/$s.o"; done
+  $CXX -std=c++20 -O2 -I"$REF/include" -I"$REPO/include" -I"$JSON_INC" -I/usr/local/cuda/include \
+    "$REPO/tests/parity/b200_collect_main.cpp" "$REPO/integration/b200_backend.cpp" "$OUT/obj_simoracle_weak.o" $others \
+    -o "$BIN2" -L"$LIBDIR" -lsk_stencil -L/usr/local/cuda/lib64 -lcudart -pthread \
+    -Wl,-rpath,"$LIBDIR" -Wl,-rpath,/usr/local/cuda/lib64
+fi
+echo "$BIN2"
