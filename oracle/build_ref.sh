@@ -64,3 +64,10 @@ if [ -f "$LIBDIR/libsk_stencil.so" ] && { [ ! -f "$BIN2" ] || [ "$REPO/integrati
     -Wl,-rpath,"$LIBDIR" -Wl,-rpath,/usr/local/cuda/lib64
 fi
 echo "$BIN2"
+
+# The reference's evaluate() on B200 sweep files (tests/parity/ref_evaluate.cpp).
+BIN3="$OUT/ref_evaluate"
+if [ ! -f "$BIN3" ] || [ "$REPO/tests/parity/ref_evaluate.cpp" -nt "$BIN3" ] || [ "$stamp" -nt "$BIN3" ]; then
+  $CXX -std=c++20 -O2 -I"$REF/include" -I"$JSON_INC" "$REPO/tests/parity/ref_evaluate.cpp" -o "$BIN3" "$stamp" -pthread
+fi
+echo "$BIN3"
