@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
 # Round-2 re-sweep with the current executor (AUTO = vector work-items where
-# they fit): the six reference kernels x all datasets, 30 observations per
+# they fit): the six reference kernels + the BASELINE configs' five_point and
+# boxmean (5,1,3,0) x all datasets, 30 observations per
 # size stored one line per observation (no means), 3 warm-ups, L2 scrubbed
 # before every sample; and the config-4 scenario (boxmean 5,1,3,0 4096^2).
 # Resumable (--resume): rerun to continue; outputs under gpurun_out/resweep.
@@ -21,6 +22,7 @@ if [ "${CONFIG4:-1}" = 1 ]; then
 fi
 timeout "${SWEEP_SECONDS:-2400}" $BIN collect --scenarios results/b200/descriptors \
   --kernel gaussian --kernel gol --kernel he --kernel nms --kernel sobel --kernel threshold \
+  --kernel five_point --kernel boxmean-5130 \
   --out $O/samples_real30.csv --refused $O/refused_real30.csv --contexts $O/contexts_real30.csv \
   --samples 30 --warmup 3 --store all --resume 2>> $O/real30_collect.log
 echo "real30 rc=$?"

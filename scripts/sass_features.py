@@ -46,7 +46,8 @@ OPCODES = {
 OP2CAT = {op: cat for cat, ops in OPCODES.items() for op in ops}
 
 KERNEL_OP = {"gaussian": "GaussianFixed<5>", "gol": "Gol", "he": "Heat", "nms": "Nms",
-             "sobel": "Sobel", "threshold": "Threshold"}
+             "sobel": "Sobel", "threshold": "Threshold", "five_point": "FivePoint",
+             "boxmean-5130": "BoxMeanFixed<5, 1, 3, 0>"}
 
 
 def sass_functions(obj: Path) -> dict[str, list[str]]:
