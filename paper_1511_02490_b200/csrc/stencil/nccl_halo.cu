@@ -118,7 +118,8 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
   if (rows < static_cast<int64_t>(N) + S) {
     return fail(SK_EINVAL, "a shard of %lld rows cannot source %d + %d halo rows", static_cast<long long>(rows), N, S);
   }
-  const Nccl& n = nccl();
+  static const Nccl none{};
+  const Nccl& n = nranks > 1 ? nccl() : none;  // one rank: no exchange, NCCL never loaded
   if (nranks > 1 && !n.ok) return fail(SK_ENOTSUP, "libnccl.so.2 not loadable: %s", dlerror());
   CommStream* cs = nullptr;
   if (int rc = comm_stream(&cs)) return rc;
