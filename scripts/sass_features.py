@@ -79,6 +79,12 @@ def main() -> int:
     funcs = sass_functions(OBJ)
 
     def counts_for(op: str) -> dict[str, int]:
+        # the kernel AUTO runs for fp32: the vector work-item instantiation
+        # when the op has one (vector.cuh), else the scalar one-pass kernel
+        vec = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024, false, 4>\(")
+        hits = [n for n in funcs if vec.match(n)]
+        if hits:
+            return categorise(funcs[hits[0]])
         want = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024(, false(, 1)?)?>\(")
         hits = [n for n in funcs if want.match(n)]
         if len(hits) != 1:
