@@ -510,6 +510,35 @@ def run_ours(args):
     elif world > 1 and args.config == "heat" and links is not None and not args.no_temporal:
         temporal = temporal_leg_sharded(args, host, shard, wc, wr, iters, world, rank)
 
+    # ---- N=1: cost of the row-shard schedule itself (interior + two boundary
+    # strips per generation, sk_stencil_iterate_nccl with one rank, no
+    # exchange) against one pass per generation - the weak-scaling ceiling of
+    # the NCCL schedule before any NVLink time (the exchange overlaps the
+    # interior)
+    shard_sched = None
+    if world == 1 and not args.no_configs:
+        from paper_1511_02490_b200.distributed import iterate_sharded_nccl
+
+        a.copy_(x0)
+        want = one_step().clone()
+        a.copy_(x0)
+        got = iterate_sharded_nccl(a, b, shard, iters, st, wc, wr)
+        exact = bool(torch.equal(shard.owned(got), shard.owned(want)))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            iterate_sharded_nccl(a, b, shard, iters, st, wc, wr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        per_gen = e0.elapsed_time(e1) / (3 * iters)
+        one_gen = ms / (args.steps * iters)
+        shard_sched = {"ms_per_generation": round(per_gen, 5), "one_pass_ms_per_generation": round(one_gen, 5),
+                       "one_pass_over_schedule": round(one_gen / per_gen, 4), "bit_exact_vs_one_pass": exact,
+                       "launches_per_generation": 3,
+                       "note": "sk_stencil_iterate_nccl at one rank (interior + 2 strips, no exchange): "
+                               "the schedule's own cost, an upper bound on weak-scaling efficiency"}
+
     # ---- the other BASELINE configs (N=1: configs 1, 3, 4; N>1: config 3)
     others = None
     if not args.no_configs:
@@ -547,6 +576,7 @@ def run_ours(args):
                          "note": "per rank, per generation (one launch at N=1)"},
             "cpu_baseline": cpu,
             "temporal_blocking": temporal,
+            "row_shard_schedule_1gpu": shard_sched,
             "configs": others,
             "e2e": e2e,
             "gpu_launches": launches,
