@@ -169,9 +169,10 @@ class RegressorBundles:
     leave-one-kernel-out for gol and he.  (The forest bundles are committed;
     a regressor's 50 variance trees over ~10^6 (scenario, size) rows are
     ~65 MB of JSON, so they are rebuilt here instead of stored.)  The study's
-    10-fold run picks the technique: on the real-kernel scenarios the speedup
-    regressor reaches 94.7 % of the oracle, the forest 93.8 %
-    (results/b200/evaluate_r02_*.txt)."""
+    10-fold run picks the technique: on its real-kernel scenarios at the
+    bench's grid sizes (8192^2, 16384^2) the speedup regressor reaches 91.4 %
+    of the oracle, the forest 89.5 % (all real kernels: 93.9 % vs 94.2 %;
+    results/b200/metrics_r02_kfold.csv.xz)."""
 
     KEYS = ("all", "gol", "he")
 
