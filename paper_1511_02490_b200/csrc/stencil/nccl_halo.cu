@@ -162,13 +162,20 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
       return fail(SK_ECUDA, "exchange wait failed");
     }
     // boundary strips: their halo rows are real data inside the grid, border
-    // cells at the global edges (rows_above / rows_below = 0 there)
+    // cells at the global edges (rows_above / rows_below = 0 there).  A
+    // strip is a few rows tall, so it runs one-row workgroups 248 cells wide
+    // (62 vector work-items of 4 cells, or 124 of 2 for fp64): the tuned
+    // wc x wr tile would be mostly rows beyond the strip - edge tiles with a
+    // fix-up pass each - for one or two useful rows.
+    const int swc = es == 8 ? 124 : 62;
     if (N > 0) {
-      if (int rc = launch(one, row(src, 0), row(dst, 0), width, N, pitch, pitch, has_n ? N : 0, S, wc, wr, st)) return rc;
+      if (int rc = launch(one, row(src, 0), row(dst, 0), width, N, pitch, pitch, has_n ? N : 0, S, swc, 1, st)) {
+        return rc;
+      }
     }
     if (S > 0) {
-      if (int rc = launch(one, row(src, rows - S), row(dst, rows - S), width, S, pitch, pitch, N, has_s ? S : 0, wc,
-                          wr, st)) {
+      if (int rc = launch(one, row(src, rows - S), row(dst, rows - S), width, S, pitch, pitch, N, has_s ? S : 0,
+                          swc, 1, st)) {
         return rc;
       }
     }
