@@ -991,7 +991,7 @@ def config4_boxmean(args, peak):
     host = _fill((4096, 4096), "float32", 0, 4)
     a = torch.from_numpy(host).cuda()
     b = torch.empty_like(a)
-    (wc, wr), best_ms, res = quick_sweep(st, a, b, 4096, 4096, top_n=16, fine_samples=30)
+    (wc, wr), best_ms, res, _, _ = quick_sweep(st, a, b, 4096, 4096, top_n=16, fine_samples=30)
     d = O.desc_from("boxmean", "float32", 5, 1, 3, 0, "nearest")
     want = O.baseline_stencil(d, host, threads=os.cpu_count() or 1)
     keys = sorted(res)
