@@ -24,7 +24,7 @@ KernelPtr vector_for_k(int K) {
     case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, 1024, false, V>);
     case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, 1024, false, V>);
     case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, false, V>);
-    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 16, 1024, false, V>);
+    default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 16, 512, false, V>);  // 128 registers
   }
 }
 
