@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -116,12 +117,23 @@ struct Session {
 std::mutex g_sess_mu;
 std::map<std::string, Session> g_sessions;
 
+std::string format_double_key(double v) {
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%a", v);
+  return buf;
+}
+
 std::string session_key(const char* model_json, const char* kernel_json, const sk_stencil_desc* d, int64_t width,
                         int64_t height) {
   int dev = 0;
   cudaGetDevice(&dev);
+  // field by field (the struct has padding bytes a caller need not zero)
   std::string key = std::string(model_json) + '\n' + kernel_json + '\n';
-  key.append(reinterpret_cast<const char*>(d), sizeof *d);
+  for (int v : {d->op, d->dtype, d->north, d->south, d->east, d->west, d->border_mode, d->complexity,
+                d->instructions, d->load_path, d->cells_per_thread, d->fused_iterations}) {
+    key += std::to_string(v) + ',';
+  }
+  key += format_double_key(d->pad_value);
   key += '\n' + std::to_string(width) + 'x' + std::to_string(height) + '@' + std::to_string(dev);
   return key;
 }
