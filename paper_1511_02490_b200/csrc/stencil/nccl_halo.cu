@@ -66,8 +66,9 @@ const Nccl& nccl() {
 
 // Per (device, calling thread): the exchange stream and its two events.
 struct CommStream {
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ready = nullptr, halo = nullptr;
+  cudaStream_t stream = nullptr;  // the exchange
+  cudaStream_t side = nullptr;    // the south strip, beside the north strip
+  cudaEvent_t ready = nullptr, halo = nullptr, south = nullptr;
 };
 std::mutex g_comm_mu;
 std::map<std::pair<int, std::thread::id>, CommStream> g_comm;
@@ -79,8 +80,10 @@ int comm_stream(CommStream** out) {
   CommStream& c = g_comm[{dev, std::this_thread::get_id()}];
   if (!c.stream) {
     if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c.halo, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c.halo, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.south, cudaEventDisableTiming) != cudaSuccess) {
       return fail(SK_ECUDA, "exchange stream/event creation failed");
     }
   }
@@ -161,6 +164,13 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
     if (nranks > 1 && cudaStreamWaitEvent(st, cs->halo, 0) != cudaSuccess) {
       return fail(SK_ECUDA, "exchange wait failed");
     }
+    // the two strips are independent, a few dozen blocks each: the south one
+    // runs on a side stream beside the north one (their latencies overlap)
+    const bool two = N > 0 && S > 0;
+    if (two && (cudaEventRecord(cs->south, st) != cudaSuccess ||
+                cudaStreamWaitEvent(cs->side, cs->south, 0) != cudaSuccess)) {
+      return fail(SK_ECUDA, "strip ordering failed");
+    }
     // boundary strips: their halo rows are real data inside the grid, border
     // cells at the global edges (rows_above / rows_below = 0 there).  A
     // strip is a few rows tall, so it runs one-row workgroups 248 cells wide
@@ -175,9 +185,13 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
     }
     if (S > 0) {
       if (int rc = launch(one, row(src, rows - S), row(dst, rows - S), width, S, pitch, pitch, N, has_s ? S : 0,
-                          swc, 1, st)) {
+                          swc, 1, two ? cs->side : st)) {
         return rc;
       }
+    }
+    if (two && (cudaEventRecord(cs->south, cs->side) != cudaSuccess ||
+                cudaStreamWaitEvent(st, cs->south, 0) != cudaSuccess)) {
+      return fail(SK_ECUDA, "strip join failed");
     }
     std::swap(src, dst);
   }
