@@ -481,6 +481,20 @@ def run_ours(args):
             return iterate_sharded_overlapped(a, b, shard, iters, st, wc, wr)
         return iterate_sharded(a, b, shard, iters, step_fn)
 
+    if nccl_abi:
+        # the C-ABI schedule needs torch's raw communicator; if this process's
+        # NCCL cannot serve it, every rank falls back to torch's send/recv
+        try:
+            one_step()
+            torch.cuda.synchronize()
+            ok = 1
+        except Exception as exc:
+            ok, why = 0, str(exc).splitlines()[0][:160]
+        flag = torch.tensor([ok], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag[0]) == 0:
+            nccl_abi = False
+            transport = "nccl (torch send/recv; C-ABI schedule unavailable" + (f": {why})" if not ok else ")")
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
