@@ -16,14 +16,14 @@ KernelPair pair_for() {
           reinterpret_cast<KernelPtr>(&k_stencil_explicit<Op, T, K, 1024>)};
 }
 
-template <class Op, typename T>
+template <class Op, typename T, int MAXT = 1024>
 KernelPtr vector_for_k(int K) {
   constexpr int V = 16 / sizeof(T);
   switch (K) {
-    case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, 1024, false, V>);
-    case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, 1024, false, V>);
-    case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, 1024, false, V>);
-    case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, 1024, false, V>);
+    case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, MAXT, false, V>);
+    case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, MAXT, false, V>);
+    case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, MAXT, false, V>);
+    case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, MAXT, false, V>);
     default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 16, 512, false, V>);  // 128 registers
   }
 }

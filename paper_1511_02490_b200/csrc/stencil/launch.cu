@@ -422,7 +422,11 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
       const long long box_w = (lw_ + ((-d.west) & (vec_ - 1)) + vec_ - 1) / vec_ * vec_;
       const bool aligned = (pitch_in * es_) % 16 == 0 && (pitch_out * es_) % 16 == 0 &&
                            (in == nullptr || reinterpret_cast<uintptr_t>(in) % 16 == 0);
-      if (d.load_path == SK_LOAD_VECTOR || (box_w <= 256 && aligned)) {
+      // AUTO also needs the block to fit the vector kernel's own thread bound
+      KernelAttr va;
+      if (int rc = kernel_attr(dev, vk, info, &va)) return rc;
+      const bool fits = static_cast<long long>(wc) * wr <= va.max_threads;
+      if (d.load_path == SK_LOAD_VECTOR || (box_w <= 256 && aligned && fits)) {
         vec_path = true;
         V = vec_;
         kp.tma = vk;
