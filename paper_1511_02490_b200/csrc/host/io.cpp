@@ -4,7 +4,7 @@
 
 #include <algorithm>
 #include <charconv>
-#include <fstream>
+#include <cstdio>
 #include <sstream>
 
 namespace wgtb {
@@ -111,51 +111,67 @@ std::vector<T> load_dir(const fs::path& dir, FromJson&& from_json) {
 }  // namespace
 
 std::string read_text(const fs::path& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw IoError("cannot open " + path.string());
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return ss.str();
+  std::error_code ec;
+  const auto size = fs::file_size(path, ec);
+  std::FILE* f = ec ? nullptr : std::fopen(path.c_str(), "rb");
+  if (!f) throw IoError(path.string() + ": cannot be opened for reading");
+  std::string text(size, '\0');
+  const std::size_t got = size ? std::fread(text.data(), 1, size, f) : 0;
+  std::fclose(f);
+  if (got != size) throw IoError(path.string() + ": short read");
+  return text;
 }
 
 void write_text(const fs::path& path, const std::string& text) {
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw IoError("cannot write " + path.string());
-  out << text;
-  if (!out) throw IoError("write failed for " + path.string());
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw IoError(path.string() + ": cannot be opened for writing");
+  const std::size_t put = std::fwrite(text.data(), 1, text.size(), f);
+  const bool closed = std::fclose(f) == 0;
+  if (put != text.size() || !closed) throw IoError(path.string() + ": write failed");
 }
 
 // ---------------------------------------------------------------- samples
+// "<id>,<w_c>,<w_r>" - the leading columns of every samples / refused line
+static std::string case_key(const std::string& id, WorkgroupSize w) {
+  std::string k = id;
+  k += ',';
+  k += std::to_string(w.cols());
+  k += ',';
+  k += std::to_string(w.rows());
+  return k;
+}
+
 std::string samples_to_csv(const SampleTable& table) {
   std::string out(kSamplesHeader);
-  out += '\n';
+  out.push_back('\n');
   for (const auto& [id, sizes] : table.rows()) {
     for (const auto& [w, runs] : sizes) {
-      const std::string key = id + ',' + std::to_string(w.cols()) + ',' + std::to_string(w.rows()) + ',';
-      for (double t : runs) out.append(key).append(format_double(t)).append("\n");
+      const std::string key = case_key(id, w);
+      for (double t : runs) (out += key) += ',' + format_double(t) + '\n';
     }
   }
   return out;
 }
 
+// Lines of one test case must be contiguous (datastore.cpp:21-25): a case
+// that was already started and then left may not start again.
 SampleTable samples_from_csv(const std::string& text) {
   SampleTable table;
-  std::set<std::pair<std::string, WorkgroupSize>> closed;
-  std::pair<std::string, WorkgroupSize> open_key;
-  bool have_open = false;
+  std::string cur_id;
+  WorkgroupSize cur_w;
+  bool started = false;
   parse_samples(text, [&](std::string id, WorkgroupSize w, double ms, std::size_t line) {
-    auto key = std::make_pair(std::move(id), w);
-    if (!have_open || key != open_key) {
-      // a group may not reappear once another group has started
-      if (closed.contains(key)) {
-        throw DuplicateTestCase("duplicate test case " + key.first + " " + w.str() + " (line " +
-                                std::to_string(line) + ")");
+    const bool same = started && w == cur_w && id == cur_id;
+    if (!same) {
+      if (table.has(id, w)) {
+        throw DuplicateTestCase("test case " + id + " " + w.str() + " reappears on line " + std::to_string(line) +
+                                " after other cases");
       }
-      if (have_open) closed.insert(open_key);
-      open_key = key;
-      have_open = true;
+      cur_id = id;
+      cur_w = w;
+      started = true;
     }
-    table.add_runtime(key.first, w, ms);
+    table.add_runtime(id, w, ms);
   });
   return table;
 }
@@ -166,11 +182,9 @@ SampleTable load_samples(const fs::path& p) { return samples_from_csv(read_text(
 // ---------------------------------------------------------------- refused
 std::string refused_to_csv(const RefusedRecord& refused) {
   std::string out(kRefusedHeader);
-  out += '\n';
+  out.push_back('\n');
   for (const auto& [id, sizes] : refused) {
-    for (const WorkgroupSize& w : sizes) {
-      out += id + ',' + std::to_string(w.cols()) + ',' + std::to_string(w.rows()) + '\n';
-    }
+    for (const WorkgroupSize& w : sizes) (out += case_key(id, w)) += '\n';
   }
   return out;
 }
@@ -216,93 +230,129 @@ ContextRecord load_contexts(const fs::path& p, const RefusedRecord& refused) {
 }
 
 // ------------------------------------------------------------ descriptors
-json device_to_json(const DeviceDescriptor& d) {
-  return json{{"id", d.id},
-              {"device_type", to_string(d.device_type)},
-              {"vendor_class", to_string(d.vendor_class)},
-              {"compute_units", d.compute_units},
-              {"frequency_mhz", d.frequency_mhz},
-              {"local_mem_kb", d.local_mem_kb},
-              {"global_cache_kb", d.global_cache_kb},
-              {"global_mem_mb", d.global_mem_mb},
-              {"device_max_wgsize", d.device_max_wgsize},
-              {"simd_width", d.simd_width}};
+// The integer fields of each descriptor as (JSON key, member) tables: one
+// loop writes them, one reads them back.  nlohmann::json objects are ordered
+// by key, so the dumped text is the reference's byte for byte.
+namespace {
+
+constexpr std::pair<const char*, int DeviceDescriptor::*> kDeviceInts[] = {
+    {"compute_units", &DeviceDescriptor::compute_units},     {"frequency_mhz", &DeviceDescriptor::frequency_mhz},
+    {"local_mem_kb", &DeviceDescriptor::local_mem_kb},       {"global_cache_kb", &DeviceDescriptor::global_cache_kb},
+    {"global_mem_mb", &DeviceDescriptor::global_mem_mb},     {"device_max_wgsize", &DeviceDescriptor::device_max_wgsize},
+    {"simd_width", &DeviceDescriptor::simd_width},
+};
+constexpr std::pair<const char*, int KernelDescriptor::*> kKernelInts[] = {
+    {"north", &KernelDescriptor::north}, {"south", &KernelDescriptor::south},
+    {"east", &KernelDescriptor::east},   {"west", &KernelDescriptor::west},
+    {"total_instructions", &KernelDescriptor::total_instructions},
+};
+constexpr std::pair<const char*, int DatasetDescriptor::*> kDatasetInts[] = {
+    {"width", &DatasetDescriptor::width}, {"height", &DatasetDescriptor::height}};
+
+template <typename D, std::size_t N>
+void put_ints(json& j, const D& d, const std::pair<const char*, int D::*> (&fields)[N]) {
+  for (const auto& [key, member] : fields) j[key] = d.*member;
 }
+
+template <typename D, std::size_t N>
+void get_ints(const json& j, D& d, const std::pair<const char*, int D::*> (&fields)[N]) {
+  for (const auto& [key, member] : fields) d.*member = j.at(key).template get<int>();
+}
+
+std::string category_key(int i) { return std::string(to_string(static_cast<InstrCategory>(i))); }
+
+std::string dataset_stem(const DatasetDescriptor& d) {
+  std::string stem = std::to_string(d.width);
+  stem += 'x';
+  stem += std::to_string(d.height);
+  stem += '-';
+  stem += to_string(d.in_type);
+  stem += '-';
+  stem += to_string(d.out_type);
+  return stem;
+}
+
+}  // namespace
+
+json device_to_json(const DeviceDescriptor& d) {
+  json j = json::object();
+  j["id"] = d.id;
+  j["device_type"] = to_string(d.device_type);
+  j["vendor_class"] = to_string(d.vendor_class);
+  put_ints(j, d, kDeviceInts);
+  return j;
+}
+
+static std::string text_of(const json& j, const char* key) { return j.at(key).get<std::string>(); }
 
 DeviceDescriptor device_from_json(const json& j) {
   DeviceDescriptor d;
-  d.id = j.at("id").get<std::string>();
-  d.device_type = device_type_from_string(j.at("device_type").get<std::string>());
-  d.vendor_class = vendor_class_from_string(j.at("vendor_class").get<std::string>());
-  j.at("compute_units").get_to(d.compute_units);
-  j.at("frequency_mhz").get_to(d.frequency_mhz);
-  j.at("local_mem_kb").get_to(d.local_mem_kb);
-  j.at("global_cache_kb").get_to(d.global_cache_kb);
-  j.at("global_mem_mb").get_to(d.global_mem_mb);
-  j.at("device_max_wgsize").get_to(d.device_max_wgsize);
-  j.at("simd_width").get_to(d.simd_width);
+  d.id = text_of(j, "id");
+  d.device_type = device_type_from_string(text_of(j, "device_type"));
+  d.vendor_class = vendor_class_from_string(text_of(j, "vendor_class"));
+  get_ints(j, d, kDeviceInts);
   d.validate();
   return d;
 }
 
 json kernel_to_json(const KernelDescriptor& k) {
-  json counts = json::object();
-  for (int i = 0; i < kInstrCategoryCount; ++i) {
-    counts[std::string(to_string(static_cast<InstrCategory>(i)))] = k.instr_counts[static_cast<std::size_t>(i)];
-  }
-  return json{{"name", k.name},   {"north", k.north}, {"south", k.south},
-              {"east", k.east},   {"west", k.west},   {"instr_counts", counts},
-              {"total_instructions", k.total_instructions}, {"complexity", k.complexity}};
+  json j = json::object();
+  j["name"] = k.name;
+  j["complexity"] = k.complexity;
+  put_ints(j, k, kKernelInts);
+  json& counts = j["instr_counts"] = json::object();
+  for (int i = 0; i < kInstrCategoryCount; ++i) counts[category_key(i)] = k.instr_counts[static_cast<std::size_t>(i)];
+  return j;
 }
 
 KernelDescriptor kernel_from_json(const json& j) {
   KernelDescriptor k;
-  k.name = j.at("name").get<std::string>();
-  j.at("north").get_to(k.north);
-  j.at("south").get_to(k.south);
-  j.at("east").get_to(k.east);
-  j.at("west").get_to(k.west);
+  k.name = text_of(j, "name");
+  k.complexity = j.at("complexity").get<bool>();
+  get_ints(j, k, kKernelInts);
+  const json& counts = j.at("instr_counts");
   for (int i = 0; i < kInstrCategoryCount; ++i) {
-    k.instr_counts[static_cast<std::size_t>(i)] =
-        j.at("instr_counts").at(std::string(to_string(static_cast<InstrCategory>(i)))).get<int>();
+    k.instr_counts[static_cast<std::size_t>(i)] = counts.at(category_key(i)).get<int>();
   }
-  j.at("total_instructions").get_to(k.total_instructions);
-  j.at("complexity").get_to(k.complexity);
   k.validate();
   return k;
 }
 
 json dataset_to_json(const DatasetDescriptor& d) {
-  return json{{"width", d.width}, {"height", d.height}, {"in_type", to_string(d.in_type)},
-              {"out_type", to_string(d.out_type)}};
+  json j = json::object();
+  put_ints(j, d, kDatasetInts);
+  j["in_type"] = to_string(d.in_type);
+  j["out_type"] = to_string(d.out_type);
+  return j;
 }
 
 DatasetDescriptor dataset_from_json(const json& j) {
   DatasetDescriptor d;
-  j.at("width").get_to(d.width);
-  j.at("height").get_to(d.height);
-  d.in_type = element_type_from_string(j.at("in_type").get<std::string>());
-  d.out_type = element_type_from_string(j.at("out_type").get<std::string>());
+  get_ints(j, d, kDatasetInts);
+  d.in_type = element_type_from_string(text_of(j, "in_type"));
+  d.out_type = element_type_from_string(text_of(j, "out_type"));
   d.validate();
   return d;
 }
 
 void save_descriptors(const DescriptorSet& set, const fs::path& dir) {
-  for (const char* sub : {"devices", "kernels", "datasets"}) fs::create_directories(dir / sub);
+  auto put = [&](const char* sub, const std::string& stem, const json& j) {
+    fs::create_directories(dir / sub);
+    write_text(dir / sub / (stem + ".json"), j.dump(2) + "\n");
+  };
   for (const auto& d : set.devices) {
     d.validate();
-    write_text(dir / "devices" / (d.id + ".json"), device_to_json(d).dump(2) + "\n");
+    put("devices", d.id, device_to_json(d));
   }
   for (const auto& k : set.kernels) {
     k.validate();
-    write_text(dir / "kernels" / (k.name + ".json"), kernel_to_json(k).dump(2) + "\n");
+    put("kernels", k.name, kernel_to_json(k));
   }
   for (const auto& d : set.datasets) {
     d.validate();
-    const std::string stem = std::to_string(d.width) + "x" + std::to_string(d.height) + "-" +
-                             std::string(to_string(d.in_type)) + "-" + std::string(to_string(d.out_type));
-    write_text(dir / "datasets" / (stem + ".json"), dataset_to_json(d).dump(2) + "\n");
+    put("datasets", dataset_stem(d), dataset_to_json(d));
   }
+  for (const char* sub : {"devices", "kernels", "datasets"}) fs::create_directories(dir / sub);
 }
 
 DescriptorSet load_descriptors(const fs::path& dir) {
@@ -313,15 +363,17 @@ DescriptorSet load_descriptors(const fs::path& dir) {
   return s;
 }
 
+// Every (device, kernel, dataset) combination, in scenario-id order.
 std::vector<Scenario> cross_scenarios(const DescriptorSet& set) {
-  std::vector<Scenario> out;
-  for (const auto& d : set.devices) {
-    for (const auto& k : set.kernels) {
-      for (const auto& ds : set.datasets) out.push_back(make_scenario(d, k, ds));
-    }
+  std::vector<Scenario> all;
+  all.reserve(set.devices.size() * set.kernels.size() * set.datasets.size());
+  for (std::size_t n = 0; n < all.capacity(); ++n) {
+    const std::size_t ds = n % set.datasets.size(), rest = n / set.datasets.size();
+    all.push_back(make_scenario(set.devices[rest / set.kernels.size()], set.kernels[rest % set.kernels.size()],
+                                set.datasets[ds]));
   }
-  std::sort(out.begin(), out.end(), [](const Scenario& a, const Scenario& b) { return a.id < b.id; });
-  return out;
+  std::ranges::sort(all, {}, &Scenario::id);
+  return all;
 }
 
 SampleTable import_external(const fs::path& csv_path, const fs::path& descriptor_dir) {
