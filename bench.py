@@ -654,7 +654,7 @@ def e2e_measure(args, st, shard, host, tdt, wc, wr, iters, world):
         h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(3)]
         for j in range(3):  # warm-up (allocates the slots' device buffers)
             st.wait_host(st.submit_host(h_in[j], h_out[j], iters, wc, wr))
-        k = max(6, min(args.steps, 24))
+        k = max(48, args.steps)  # steady state: pipeline fill + drain amortised (scripts/e2e_probe.py)
         tickets = []
         t0 = time.perf_counter()
         for j in range(k):
