@@ -125,6 +125,21 @@ int main() {
     tb.run_host(h.data(), o2.data(), W, H, 13, 32, 12);
     CHECK(o1 == o2, "strip heat differs from one-pass");
   }
+  // vector work-items (SK_LOAD_VECTOR) through the host API equal the scalar TMA kernel
+  {
+    const int W = 264, H = 203;
+    std::vector<float> h(W * H), o1(W * H), o2(W * H);
+    for (int i = 0; i < W * H; ++i) h[i] = static_cast<float>((i * 2654435761u) % 1000) / 1000.0f;
+    wgtb::Stencil<float> vec(SK_OP_BOXMEAN, {5, 1, 3, 0}, wgtb::Border::nearest());
+    wgtb::Stencil<float> sca(SK_OP_BOXMEAN, {5, 1, 3, 0}, wgtb::Border::nearest());
+    vec.load_path(SK_LOAD_VECTOR);
+    sca.load_path(SK_LOAD_TMA);
+    vec.run_host(h.data(), o1.data(), W, H, 3, 16, 8);
+    sca.run_host(h.data(), o2.data(), W, H, 3, 32, 8);
+    CHECK(o1 == o2, "vector box mean differs from the scalar kernel");
+    int32_t km = 0;
+    CHECK(vec.probe(W, H, 16, 8, &km) == SK_OK && km >= 512, "vector probe");
+  }
   std::printf(fails ? "FAILED %d\n" : "OK\n", fails);
   return fails ? 1 : 0;
 }
