@@ -977,14 +977,16 @@ def config3_heat(args, peak):
         st.iterate(a, b, iters, wc, wr)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        st.iterate(a, b, iters, wc, wr)
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record()
+        for _ in range(steps):
+            st.iterate(a, b, iters, wc, wr)
+        e1.record()
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     g = float(H) * W * iters / (ms / 1e3) / 1e9
     return {"config3_heat_16384": {
+        "clocks": clk.summary(),
         "value": round(g, 2), "unit": "Gcells/s", "ms_per_step": round(ms, 3),
         "iterations_per_step": iters, "steps": steps, "block": f"{wc}x{wr}",
         "hbm_frac": round(g * 8 / peak, 4), "parity": exact, "parity_generations": gens,
