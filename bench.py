@@ -323,11 +323,19 @@ def tune_block(st, config, a, b, W, H, gens=0):
     iter_timer = None
     if gens > 0:
         iter_timer = pass_timer(st, a, b, gens)
-        it = {k: iter_timer(k[0], k[1], 3) for k in fine}
+        # round-robin over the candidates so they share the device's power
+        # state (sustained streaming reaches the power cap: heat 16384^2 draws
+        # ~1 kW), then the median of each candidate's samples
+        runs = {k: [] for k in fine}
+        for _ in range(3):
+            for k in fine:
+                runs[k].append(iter_timer(k[0], k[1], 1))
+        it = {k: float(np.median(v)) for k, v in runs.items()}
         wbest = min(it, key=lambda k: (it[k], k))
         info["workload_block"] = f"{wbest[0]}x{wbest[1]}"
         info["workload_ms_per_generation"] = round(it[wbest], 5)
-        info["workload_timing"] = f"the sweep's top {len(fine)} sizes, {gens} iterated generations x 3"
+        info["workload_timing"] = (f"the sweep's top {len(fine)} sizes, {gens} iterated generations, "
+                                   "3 round-robin samples each, median")
     info["sweep_s"] = round(time.time() - t0, 1)
 
     def perf_of(pred):
