@@ -1029,7 +1029,14 @@ def config4_boxmean(args, peak):
         if b.cpu().numpy().tobytes() != want.tobytes():
             bad.append(f"{k[0]}x{k[1]}")
     g = 4096 * 4096 / (best_ms / 1e3) / 1e9
+    # the oracle block's distribution over 30 fresh samples (SURVEY.md §8d:
+    # mean as the estimator, median and p10/p90 beside it)
+    obs = np.array(st.time(a, b, wc, wr, samples=30, warmup=3, flush_l2=True)) * 1e3
+    dist_us = {"mean": round(float(obs.mean()), 2), "median": round(float(np.median(obs)), 2),
+               "p10": round(float(np.percentile(obs, 10)), 2), "p90": round(float(np.percentile(obs, 90)), 2),
+               "samples": int(obs.size)}
     return {"config4_boxmean5130_4096": {
+        "oracle_pass_us_distribution": dist_us,
         "oracle_block": f"{wc}x{wr}", "oracle_pass_us": round(best_ms * 1e3, 2),
         "value": round(g, 1), "unit": "Gcells/s", "hbm_frac": round(g * 8 / peak, 4),
         "sizes_timed": len(res), "oracle_over_worst": round(max(res.values()) / best_ms, 2),
