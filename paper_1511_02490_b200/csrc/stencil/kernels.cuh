@@ -379,6 +379,14 @@ __global__ void __launch_bounds__(MAXT)
     }
     fence_barrier_init();
     fence_proxy_async_smem();
+    // Programmatic dependent launch (launch.cu: launch_tma): everything above
+    // touches only shared memory and the tensor map, so it overlaps the tail
+    // of the previous generation's kernel; no global read or write happens
+    // before that kernel has completed and its stores are visible.  Then let
+    // the next generation's CTAs be scheduled onto SMs as ours retire.
+    // (Without a programmatic dependency both instructions are no-ops.)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int s = 0; s < g.stages; ++s) {
       int t = blockIdx.x + s * gridDim.x;
       if (t < ntiles) {

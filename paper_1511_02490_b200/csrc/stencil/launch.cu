@@ -42,6 +42,29 @@ bool is_config_error(cudaError_t e) {
   return e == cudaErrorInvalidConfiguration || e == cudaErrorLaunchOutOfResources;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+cudaError_t launch_tma(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
+  if (!pdl_enabled()) return cudaLaunchKernel(kernel, grid, block, args, smem, stream);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, kernel, args);
+}
+
 int launch_error(cudaError_t e) {
   if (is_config_error(e)) {
     cudaGetLastError();

@@ -34,6 +34,10 @@ int fail(int code, const char* fmt, ...);
 bool is_config_error(cudaError_t e);
 // Status for a failed launch: SK_REFUSED / SK_EINVAL / SK_ECUDA.
 int launch_error(cudaError_t e);
+// A one-pass TMA kernel launched with programmatic stream serialization
+// (PDL): its prologue may overlap the previous kernel's tail; the kernel
+// waits (griddepcontrol.wait) before any global access.  SK_PDL=0 disables.
+cudaError_t launch_tma(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream);
 size_t dtype_size(int dtype);
 
 // ---------------------------------------------------------- device facts
@@ -210,7 +214,7 @@ inline int launch_typed(const sk_stencil_desc& d, const Plan& plan, const void* 
     if (int rc = tensor_map(key, &map)) return rc;
     void* args[] = {&map, &out, const_cast<Geom*>(&plan.g), &pad, &p};
     if (plan.driver_handle) return launch_driver(plan, dim3(plan.grid), block, args, stream);
-    e = cudaLaunchKernel(plan.kernel, dim3(plan.grid), block, args, plan.smem, stream);
+    e = launch_tma(plan.kernel, dim3(plan.grid), block, args, plan.smem, stream);
   } else {
     const T* tin = static_cast<const T*>(in);
     T* tout = static_cast<T*>(out);
