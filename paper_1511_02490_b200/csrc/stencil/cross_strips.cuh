@@ -206,6 +206,10 @@ template <class Op, typename T, int R>
 __global__ void __launch_bounds__(CrossBounds<R>::kThreads, CrossBounds<R>::kMinBlocks)
     k_cross_strips(const T* __restrict__ in, T* __restrict__ out, const CrossGeom g, const T pad,
                    const __grid_constant__ OpParams<T> p) {
+  // programmatic dependent launch (launch.cu: launch_pdl_checked): no global
+  // access before the previous launch has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char sm_raw[];
   Quad<T>* xchg = reinterpret_cast<Quad<T>*>(sm_raw);  // [2 parities][nwarps][top, bottom][32]
   const int lane = threadIdx.x & 31;

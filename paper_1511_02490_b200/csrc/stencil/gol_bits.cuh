@@ -171,6 +171,10 @@ __device__ __forceinline__ void strips_substitute(uint32_t (&w)[R], const StripG
 template <int R>
 __global__ void __launch_bounds__(R <= 8 ? 768 : (R <= 16 ? 512 : 256))
     k_gol_strips(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, const StripGeom g) {
+  // programmatic dependent launch (launch.cu: launch_pdl_checked): no global
+  // access before the previous launch has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) uint32_t sm_x[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;

@@ -65,6 +65,11 @@ cudaError_t launch_tma(const void* kernel, dim3 grid, dim3 block, void** args, i
   return cudaLaunchKernelExC(&cfg, kernel, args);
 }
 
+int launch_pdl_checked(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
+  const cudaError_t e = launch_tma(kernel, grid, block, args, smem, stream);
+  return e == cudaSuccess ? SK_OK : launch_error(e);
+}
+
 int launch_error(cudaError_t e) {
   if (is_config_error(e)) {
     cudaGetLastError();

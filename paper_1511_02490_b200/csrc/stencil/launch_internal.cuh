@@ -38,6 +38,10 @@ int launch_error(cudaError_t e);
 // (PDL): its prologue may overlap the previous kernel's tail; the kernel
 // waits (griddepcontrol.wait) before any global access.  SK_PDL=0 disables.
 cudaError_t launch_tma(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream);
+// The same for kernels that execute griddepcontrol.wait before their first
+// global access (the register-strip and bit-plane kernels), with the launch
+// status mapped like launch_checked.
+int launch_pdl_checked(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream);
 size_t dtype_size(int dtype);
 
 // ---------------------------------------------------------- device facts

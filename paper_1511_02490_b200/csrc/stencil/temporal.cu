@@ -129,8 +129,8 @@ int run_bits(const sk_stencil_desc& d, const void* in, void* out, long long W, l
     const uint32_t* src = static_cast<const uint32_t*>(P[cur]) + (firstl ? a * pw : 0);
     uint32_t* dst = static_cast<uint32_t*>(P[1 - cur]);
     void* args[] = {&src, &dst, &plan.g};
-    if (int rc = launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads),
-                                args, plan.smem, stream)) {
+    if (int rc = launch_pdl_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads),
+                                    args, plan.smem, stream)) {
       return rc;
     }
     cur = 1 - cur;
@@ -228,8 +228,8 @@ int launch_cross_typed(const sk_stencil_desc& d, const CrossPlan& plan, const vo
   const T* tin = static_cast<const T*>(in);
   T* tout = static_cast<T*>(out);
   void* args[] = {&tin, &tout, const_cast<CrossGeom*>(&plan.g), &pad, &p};
-  return launch_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads), args,
-                        plan.smem, stream);
+  return launch_pdl_checked(plan.kernel, dim3(static_cast<unsigned>(plan.grid)), dim3(plan.threads), args,
+                            plan.smem, stream);
 }
 
 // One k_cross_strips launch: `tb` generations from `in` (row 0 of the region,
