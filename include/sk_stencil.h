@@ -216,6 +216,15 @@ int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, 
                     int64_t height, int64_t pitch, int32_t wc, int32_t wr, int32_t warmup,
                     int32_t samples, int32_t flush_l2, double* ms_out);
 
+/* The streaming ceiling at a given size (no reference counterpart; the
+ * denominator beside the measured HBM peak): `samples` copies of `bytes`
+ * from d_in to d_out under exactly sk_stencil_time's harness (same stream,
+ * events and L2 scrub).  kind 0 = cudaMemcpyAsync device-to-device, kind 1 =
+ * a 16-B vector grid-stride copy kernel (16-B aligned, bytes % 16 == 0).
+ * ms_out[samples]. */
+int sk_copy_time(const void* d_in, void* d_out, int64_t bytes, int32_t kind, int32_t warmup,
+                 int32_t samples, int32_t flush_l2, double* ms_out);
+
 /* End-to-end call from HOST buffers (the plugin call a SkelCL user makes):
  * copies h_in (W*H dense) to the device, runs `iterations` passes, copies the
  * result to h_out.  Device buffers are cached per (size) inside the library. */

@@ -7,7 +7,7 @@ csrc/host.  This package is the Python mirror used by tests and bench.py.
 """
 from ._native import NativeError, lib  # noqa: F401
 from .stencil import (IllegalWorkgroupSize, RefusedParameter, Stencil,  # noqa: F401
-                      device_features, fill_host)
+                      copy_time, device_features, fill_host)
 
 __all__ = ["Stencil", "RefusedParameter", "IllegalWorkgroupSize", "NativeError", "lib",
-           "device_features", "fill_host"]
+           "copy_time", "device_features", "fill_host"]

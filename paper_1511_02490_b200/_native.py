@@ -119,6 +119,7 @@ _PROTOTYPES = {
     "sk_kernel_max_wgsize": (_i32, [_desc_p, ctypes.POINTER(_i32)]),
     "sk_stencil_time": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32,
                                ctypes.POINTER(ctypes.c_double)]),
+    "sk_copy_time": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, ctypes.POINTER(ctypes.c_double)]),
     "sk_stencil_run_host": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i32, _i32, _i32]),
     "sk_stencil_submit_host": (_i32, [_desc_p, _vp, _vp, _i64, _i64, _i32, _i32, _i32,
                                       ctypes.POINTER(_i64)]),

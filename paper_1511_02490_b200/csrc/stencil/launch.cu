@@ -1069,6 +1069,42 @@ int sk_kernel_max_wgsize(const sk_stencil_desc* desc, int32_t* kernel_max) {
   return rc;
 }
 
+namespace {
+
+int ensure_events(Scratch* s, int samples) {
+  for (int i = static_cast<int>(s->events.size()); i < 2 * samples; ++i) {
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return fail(SK_ECUDA, "cudaEventCreate failed");
+    s->events.push_back(ev);
+  }
+  return SK_OK;
+}
+
+// write 2 x L2 (evicts everything), then read it back (the written lines
+// leave dirty during this read, not during the timed pass)
+int scrub_l2(Scratch* s, int sample) {
+  cudaMemsetAsync(s->flush, sample & 0xff, s->flush_bytes, s->stream);
+  DeviceInfo info;
+  if (int rc = current_device_info(&info)) return rc;
+  k_l2_scrub<<<info.sms * 4, 512, 0, s->stream>>>(static_cast<const uint4*>(s->flush),
+                                                 static_cast<long long>(s->flush_bytes / 16),
+                                                 static_cast<unsigned*>(s->flush));
+  return SK_OK;
+}
+
+int collect_samples(Scratch* s, int samples, double* ms_out) {
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return fail(SK_ECUDA, "timing stream failed: %s", cudaGetErrorString(e));
+  for (int i = 0; i < samples; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]);
+    ms_out[i] = ms;
+  }
+  return SK_OK;
+}
+
+}  // namespace
+
 int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, int64_t width,
                     int64_t height, int64_t pitch, int32_t wc, int32_t wr, int32_t warmup,
                     int32_t samples, int32_t flush_l2, double* ms_out) {
@@ -1084,23 +1120,10 @@ int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, 
   }
   // All samples are enqueued back to back (flush, event, pass, event) and
   // synchronised once; each sample is its own event pair on the stream.
-  if (static_cast<int>(s->events.size()) < 2 * samples) {
-    for (int i = static_cast<int>(s->events.size()); i < 2 * samples; ++i) {
-      cudaEvent_t ev;
-      if (cudaEventCreate(&ev) != cudaSuccess) return fail(SK_ECUDA, "cudaEventCreate failed");
-      s->events.push_back(ev);
-    }
-  }
+  if (int rc = ensure_events(s, samples)) return rc;
   for (int i = 0; i < samples; ++i) {
     if (flush_l2) {
-      // write 2 x L2 (evicts everything), then read it back (the written
-      // lines leave dirty during this read, not during the timed pass)
-      cudaMemsetAsync(s->flush, i & 0xff, s->flush_bytes, s->stream);
-      DeviceInfo info;
-      if (int rc = current_device_info(&info)) return rc;
-      k_l2_scrub<<<info.sms * 4, 512, 0, s->stream>>>(static_cast<const uint4*>(s->flush),
-                                                     static_cast<long long>(s->flush_bytes / 16),
-                                                     static_cast<unsigned*>(s->flush));
+      if (int rc = scrub_l2(s, i)) return rc;
     }
     cudaEventRecord(s->events[2 * i], s->stream);
     if (int rc = launch(*desc, d_in, d_out, width, height, pitch, pitch, 0, 0, wc, wr, s->stream)) {
@@ -1109,14 +1132,49 @@ int sk_stencil_time(const sk_stencil_desc* desc, const void* d_in, void* d_out, 
     }
     cudaEventRecord(s->events[2 * i + 1], s->stream);
   }
-  cudaError_t e = cudaStreamSynchronize(s->stream);
-  if (e != cudaSuccess) return fail(SK_ECUDA, "timing stream failed: %s", cudaGetErrorString(e));
-  for (int i = 0; i < samples; ++i) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]);
-    ms_out[i] = ms;
+  return collect_samples(s, samples, ms_out);
+}
+
+// The streaming ceiling the one-pass kernel is held to at a given size: a
+// copy of the same bytes (read + write once), 16-B vector grid-stride loop.
+__global__ void k_copy_ceiling(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    dst[i] = src[i];
   }
-  return SK_OK;
+}
+
+int sk_copy_time(const void* d_in, void* d_out, int64_t bytes, int32_t kind, int32_t warmup,
+                 int32_t samples, int32_t flush_l2, double* ms_out) {
+  g_last_error.clear();
+  if (!d_in || !d_out || bytes < 16 || (samples > 0 && !ms_out)) return fail(SK_EINVAL, "bad argument");
+  if (kind != 0 && kind != 1) return fail(SK_EINVAL, "kind must be 0 (cudaMemcpyAsync) or 1 (copy kernel)");
+  if (kind == 1 && ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out) | bytes) & 15)) {
+    return fail(SK_EINVAL, "the copy kernel needs 16-B aligned buffers and a multiple of 16 bytes");
+  }
+  Scratch* s = nullptr;
+  if (int rc = scratch(&s)) return rc;
+  DeviceInfo info;
+  if (int rc = current_device_info(&info)) return rc;
+  auto copy = [&] {
+    if (kind == 0) {
+      cudaMemcpyAsync(d_out, d_in, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, s->stream);
+    } else {
+      k_copy_ceiling<<<info.sms * 4, 512, 0, s->stream>>>(static_cast<const uint4*>(d_in),
+                                                         static_cast<uint4*>(d_out), bytes / 16);
+    }
+  };
+  for (int i = 0; i < warmup; ++i) copy();
+  if (int rc = ensure_events(s, samples)) return rc;
+  for (int i = 0; i < samples; ++i) {
+    if (flush_l2) {
+      if (int rc = scrub_l2(s, i)) return rc;
+    }
+    cudaEventRecord(s->events[2 * i], s->stream);
+    copy();
+    cudaEventRecord(s->events[2 * i + 1], s->stream);
+  }
+  return collect_samples(s, samples, ms_out);
 }
 
 int sk_stencil_run_host(const sk_stencil_desc* desc, const void* h_in, void* h_out,

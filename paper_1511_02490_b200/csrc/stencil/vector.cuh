@@ -75,6 +75,46 @@ __device__ __forceinline__ void load_window(const T* row, T (&w)[L + V + R]) {
   }
 }
 
+// Packed fp32 pairs: sm_100's FADD2 / FMUL2 / FFMA2 issue two IEEE
+// round-to-nearest operations per instruction, each lane rounded exactly as
+// its scalar FADD / FMUL / FFMA (no flush-to-zero), so pairing two columns of
+// a work-item halves the instructions of a chain without changing a bit.
+struct F2 {
+  float x, y;
+};
+
+#define SK_F2_OP2(name, ptx)                                                                  \
+  __device__ __forceinline__ F2 name(F2 a, F2 b) {                                            \
+    F2 r;                                                                                     \
+    asm("{\n .reg .b64 a, b, r;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n " ptx        \
+        " r, a, b;\n mov.b64 {%0, %1}, r;\n}"                                                 \
+        : "=f"(r.x), "=f"(r.y)                                                                \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                            \
+    return r;                                                                                 \
+  }
+SK_F2_OP2(add2, "add.rn.f32x2")
+SK_F2_OP2(mul2, "mul.rn.f32x2")
+#undef SK_F2_OP2
+
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("{\n .reg .b64 a, b, c, r;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+      " mov.b64 c, {%6, %7};\n fma.rn.f32x2 r, a, b, c;\n mov.b64 {%0, %1}, r;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
+// div_const_fast<D> (ops.cuh) on a pair: q0 = s RN(1/D); r = q0 (-D) + s
+// (the same exact remainder as -q0 D + s); q = r RN(1/D) + q0.
+template <int D>
+__device__ __forceinline__ F2 div_const_fast2(F2 s) {
+  constexpr float y = 1.0f / static_cast<float>(D);
+  const F2 q0 = mul2(s, F2{y, y});
+  const F2 r = fma2(q0, F2{-static_cast<float>(D), -static_cast<float>(D)}, s);
+  return fma2(r, F2{y, y}, q0);
+}
+
 // Register view over a rolling window of 3 rows (north, centre, south) for
 // the generic 3x3 form: at(dr, dc) of output column j.
 template <typename T, int RW>
@@ -180,19 +220,38 @@ __device__ __forceinline__ void vblock_boxmean(const T* first, int pitch, Emit&&
   for (int k = 0; k < K; ++k) {
     row_sums(first + (k + S) * pitch, rs[NR - 1]);
     A sum[V];
+    if constexpr (std::is_same_v<T, float> && V % 2 == 0) {
+      // two columns per packed add, north to south as the scalar chain
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      A s = rs[0][j];
+      for (int j = 0; j < V; j += 2) {
+        F2 s{rs[0][j], rs[0][j + 1]};
 #pragma unroll
-      for (int i = 1; i < NR; ++i) s = acc_add2<T>(s, rs[i][j]);
-      sum[j] = s;
+        for (int i = 1; i < NR; ++i) s = add2(s, F2{rs[i][j], rs[i][j + 1]});
+        sum[j] = s.x;
+        sum[j + 1] = s.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        A s = rs[0][j];
+#pragma unroll
+        for (int i = 1; i < NR; ++i) s = acc_add2<T>(s, rs[i][j]);
+        sum[j] = s;
+      }
     }
     T out[V];
     if constexpr (std::is_same_v<T, float> && kCount == 28) {
       bool fast = true;
 #pragma unroll
       for (int j = 0; j < V; ++j) fast = fast && div_const_in_range(sum[j]);
-      if (fast) {
+      if (fast && V % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j + 1 < V; j += 2) {
+          const F2 q = div_const_fast2<kCount>(F2{sum[j], sum[j + 1]});
+          out[j] = q.x;
+          out[j + 1] = q.y;
+        }
+      } else if (fast) {
 #pragma unroll
         for (int j = 0; j < V; ++j) out[j] = div_const_fast<kCount>(sum[j]);
       } else {

@@ -278,6 +278,23 @@ def device_features(device: int = 0) -> dict:
     return out
 
 
+def copy_time(src, dst, samples: int = 30, warmup: int = 3, flush_l2: bool = True,
+              kind: str = "kernel") -> list[float]:
+    """The streaming ceiling at a given size: ``samples`` timed copies (ms) of
+    ``src`` into ``dst`` (device tensors of equal size) under
+    ``Stencil.time``'s harness - same stream, events and L2 scrub.  ``kind``
+    "kernel" is a 16-B vector copy kernel, "memcpy" cudaMemcpyAsync."""
+    if src.device.type != "cuda" or dst.device != src.device:
+        raise ValueError("copy_time needs two tensors on the same CUDA device")
+    nbytes = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() != nbytes or not (src.is_contiguous() and dst.is_contiguous()):
+        raise ValueError("copy_time needs contiguous tensors of equal size")
+    ms = (ctypes.c_double * max(samples, 1))()
+    N.check(N.lib().sk_copy_time(src.data_ptr(), dst.data_ptr(), nbytes, {"memcpy": 0, "kernel": 1}[kind],
+                                 warmup, samples, int(flush_l2), ms), "sk_copy_time")
+    return list(ms[:samples])
+
+
 def fill_host(arr, kind: int, seed: int) -> None:
     """Deterministic reference-Rng input (mt19937_64, rng.hpp:34-72) into a host array."""
     import numpy as np

@@ -227,6 +227,21 @@ def test_timing_returns_positive_samples():
     assert len(ms) == 5 and all(t > 0 for t in ms)
 
 
+def test_copy_ceiling_copies_and_times():
+    """sk_copy_time: both kinds copy the bytes exactly, timed under the same
+    harness as sk_stencil_time; misaligned kernel copies are EINVAL."""
+    from paper_1511_02490_b200 import NativeError, copy_time
+
+    a = to_dev(rand_grid("float32", (1024, 1024), 7))
+    for kind in ("kernel", "memcpy"):
+        b = torch.zeros_like(a)
+        ms = copy_time(a, b, samples=4, warmup=1, kind=kind)
+        assert len(ms) == 4 and all(t > 0 for t in ms)
+        assert torch.equal(a, b)
+    with pytest.raises(NativeError):
+        copy_time(a.view(-1)[1:-3], torch.empty_like(a).view(-1)[:-4], samples=1, kind="kernel")
+
+
 def test_run_host_end_to_end():
     st = Stencil(op="gol", dtype="int32")
     x = rand_grid("int32", (256, 300), 4, "gol")
