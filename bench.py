@@ -382,6 +382,24 @@ def tune_block(st, config, a, b, W, H, gens=0):
     # (leave-one-kernel-out), so the prediction is not in-sample
     info["held_out"] = predicted(True, "forest")
     info["held_out_speedup_reg"] = predicted(True, "speedup-reg")
+    # B200 refinement (no reference counterpart): the forest's 8-size
+    # shortlist timed live (wgtb_tune_measured), 8 x 4 passes instead of
+    # the sweep's 1,466 sizes; in-sample and held out
+    def measured(held_out):
+        from paper_1511_02490_b200 import autotune
+
+        kname = "he" if config == "heat" else config
+        kernel = ROOT / "results" / "b200" / "descriptors" / "kernels" / f"{kname}.json"
+        model = ROOT / "results" / "b200" / (f"model_loko_{kname}.json" if held_out else "model.json")
+        if not (model.exists() and kernel.exists()):
+            return {"predicted_over_oracle": None, "prediction_note": f"no trained model bundle ({model})"}
+        r = autotune.tune_measured(st, a, b, kernel, model, n=8, samples=3)
+        pms, p = perf_of((r["wc"], r["wr"]))
+        return {"block": f"{r['wc']}x{r['wr']}", "sizes_timed": r["timed"], "tuning_ms": round(r["ms"], 2),
+                "pass_ms": round(pms, 5), "over_oracle": p}
+
+    info["measured_shortlist"] = {"technique": "forest-nn shortlist (vote order) x live timing, 8 sizes",
+                                  "in_sample": measured(False), "held_out": measured(True)}
     if _BUNDLES is not None:
         info["regressor_training_s"] = _BUNDLES.seconds
     # the human-expert and common fixed sizes (bench.cpp:550-566)

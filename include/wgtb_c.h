@@ -26,6 +26,27 @@ int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stenc
                  int64_t width, int64_t height, int32_t* wc, int32_t* wr, int32_t* probes,
                  double* elapsed_ms);
 
+/* The model's shortlist for (desc, W, H, current device), best first: up to
+ * max_n sizes legal on the device - Algorithm 1/2's own answer (what
+ * wgtb_predict returns), then the rest of the model's ranking (a forest's
+ * labels by vote count, a regressor's sizes by predicted fitness), then that
+ * answer's nearest legal neighbours.  wcs / wrs hold max_n entries; *n_out
+ * the count written.  No reference counterpart: the paper returns one size. */
+int wgtb_shortlist(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc, int64_t width,
+                   int64_t height, int32_t max_n, int32_t* wcs, int32_t* wrs, int32_t* n_out);
+
+/* Prediction refined by measurement: every size of the model's shortlist
+ * (wgtb_shortlist, max_n sizes) timed on d_in -> d_out with sk_stencil_time
+ * (`samples` flushed passes, median); the fastest is returned in *wc / *wr
+ * with its median in *best_ms.  max_n = 1 times wgtb_predict's answer only.
+ * *timed: sizes timed; *elapsed_ms: the whole tuning time (model + timing).
+ * Costs max_n * (samples + 1) passes instead of the exhaustive sweep's
+ * 1,466 sizes. */
+int wgtb_tune_measured(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                       const void* d_in, void* d_out, int64_t width, int64_t height, int64_t pitch,
+                       int32_t max_n, int32_t samples, int32_t* wc, int32_t* wr, int32_t* timed, double* best_ms,
+                       double* elapsed_ms);
+
 /* Online tuning (the paper's runtime loop; the reference
  * daemon's session, serve.cpp:123-164): one stencil pass with the size the
  * model proposes for (desc, W, H, current device).  The proposal is cached

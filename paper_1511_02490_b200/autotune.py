@@ -25,6 +25,18 @@ def lib():
                                    ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_double)]
+        h.wgtb_shortlist.restype = ctypes.c_int
+        h.wgtb_shortlist.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(N.sk_stencil_desc),
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int32)]
+        h.wgtb_tune_measured.restype = ctypes.c_int
+        h.wgtb_tune_measured.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(N.sk_stencil_desc),
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
         h.wgtb_launch_tuned.restype = ctypes.c_int
         h.wgtb_launch_tuned.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(N.sk_stencil_desc),
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
@@ -51,6 +63,36 @@ def predict(stencil, width: int, height: int, kernel_json: str | Path,
     if rc != 0:
         raise RuntimeError(f"wgtb_predict: {lib().wgtb_last_error().decode()}")
     return {"wc": wc.value, "wr": wr.value, "probes": probes.value, "ms": ms.value}
+
+
+def shortlist(stencil, width: int, height: int, kernel_json: str | Path,
+              model_json: str | Path = RESULTS / "model.json", n: int = 8) -> list[tuple[int, int]]:
+    """The model's n best-ranked sizes legal on the current device, best
+    first; the first is predict()'s answer (wgtb_shortlist)."""
+    wcs, wrs, got = (ctypes.c_int32 * n)(), (ctypes.c_int32 * n)(), ctypes.c_int32()
+    rc = lib().wgtb_shortlist(str(model_json).encode(), str(kernel_json).encode(), ctypes.byref(stencil.desc),
+                              width, height, n, wcs, wrs, ctypes.byref(got))
+    if rc != 0:
+        raise RuntimeError(f"wgtb_shortlist: {lib().wgtb_last_error().decode()}")
+    return [(wcs[i], wrs[i]) for i in range(got.value)]
+
+
+def tune_measured(stencil, inp, out, kernel_json: str | Path, model_json: str | Path = RESULTS / "model.json",
+                  n: int = 8, samples: int = 5) -> dict:
+    """Prediction refined by measurement (wgtb_tune_measured): the model's
+    n-size shortlist timed on inp -> out (median of `samples` flushed
+    passes each); {'wc', 'wr', 'timed', 'best_ms', 'ms'} of the fastest."""
+    stencil._check_device(inp, out)
+    h, w = out.shape
+    wc, wr, timed = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    best, ms = ctypes.c_double(), ctypes.c_double()
+    rc = lib().wgtb_tune_measured(str(model_json).encode(), str(kernel_json).encode(), ctypes.byref(stencil.desc),
+                                  inp.data_ptr(), out.data_ptr(), w, h, inp.stride(0), n, samples,
+                                  ctypes.byref(wc), ctypes.byref(wr), ctypes.byref(timed), ctypes.byref(best),
+                                  ctypes.byref(ms))
+    if rc != 0:
+        raise RuntimeError(f"wgtb_tune_measured: {lib().wgtb_last_error().decode()}")
+    return {"wc": wc.value, "wr": wr.value, "timed": timed.value, "best_ms": best.value, "ms": ms.value}
 
 
 class Tuned:

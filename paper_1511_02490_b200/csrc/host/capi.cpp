@@ -1,11 +1,13 @@
 // extern "C" entry points of libwgtb (include/wgtb_c.h).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <vector>
 
 #include "wgtb/autotune.hpp"
 #include "wgtb/io.hpp"
@@ -169,11 +171,101 @@ void propose(Session& s, const sk_stencil_desc* desc, int64_t width, int64_t hei
   ++s.proposals;
 }
 
+// Live legality of one size for the scene's stencil.
+wgtb::ProbeResult device_probe(const sk_stencil_desc* desc, int64_t width, int64_t height, wgtb::WorkgroupSize w) {
+  const int rc = sk_stencil_probe(desc, width, height, w.cols(), w.rows(), nullptr, nullptr, nullptr);
+  if (rc == SK_OK) return wgtb::ProbeResult::Legal;
+  if (rc == SK_OVERSIZED) return wgtb::ProbeResult::Oversized;
+  if (rc == SK_REFUSED) return wgtb::ProbeResult::Refused;
+  throw wgtb::DeviceError(sk_last_error());
+}
+
+// The model's shortlist for a scene (autotune.hpp: shortlist_*), with live
+// device probes; *probes counts them.
+std::vector<wgtb::WorkgroupSize> shortlist(const Scene& sc, const sk_stencil_desc* desc, int64_t width,
+                                           int64_t height, int n, int* probes) {
+  const Bundle& b = *sc.bundle;
+  const auto ctx = session_context(b, sc.scenario.device.device_max_wgsize, sc.kmax, {});
+  const wgtb::ProbeFn probe = [&](wgtb::WorkgroupSize w) {
+    ++*probes;
+    return device_probe(desc, width, height, w);
+  };
+  if (b.regressor) {
+    const auto fm = b.regressor->mode() == wgtb::RegressionMode::Runtime ? wgtb::FitnessMode::RuntimeReciprocal
+                                                                         : wgtb::FitnessMode::Speedup;
+    return wgtb::shortlist_regress(*b.regressor, sc.features, ctx, fm, probe, n);
+  }
+  const auto strategy = b.fallback == "random" ? wgtb::FallbackStrategy::random(wgtb::fnv1a64(sc.scenario.id, 0))
+                                               : wgtb::FallbackStrategy::nearest_neighbour();
+  return wgtb::shortlist_classify(*b.classifier, sc.features, ctx, strategy, probe, n);
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* wgtb_last_error(void) { return g_error.c_str(); }
+
+int wgtb_shortlist(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc, int64_t width,
+                   int64_t height, int32_t max_n, int32_t* wcs, int32_t* wrs, int32_t* n_out) {
+  g_error.clear();
+  try {
+    if (!wcs || !wrs || !n_out || max_n < 1) throw wgtb::InvalidArgument("null argument or max_n < 1");
+    const Scene sc = make_scene(model_json, kernel_json, desc, width, height);
+    int probes = 0;
+    const auto list = shortlist(sc, desc, width, height, max_n, &probes);
+    for (std::size_t i = 0; i < list.size(); ++i) {
+      wcs[i] = list[i].cols();
+      wrs[i] = list[i].rows();
+    }
+    *n_out = static_cast<int32_t>(list.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1;
+  }
+}
+
+int wgtb_tune_measured(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
+                       const void* d_in, void* d_out, int64_t width, int64_t height, int64_t pitch,
+                       int32_t max_n, int32_t samples, int32_t* wc, int32_t* wr, int32_t* timed, double* best_ms,
+                       double* elapsed_ms) {
+  g_error.clear();
+  try {
+    if (!wc || !wr || max_n < 1 || samples < 1) throw wgtb::InvalidArgument("null argument, max_n or samples < 1");
+    const auto t0 = std::chrono::steady_clock::now();
+    const Scene sc = make_scene(model_json, kernel_json, desc, width, height);
+    int probes = 0;
+    const auto list = shortlist(sc, desc, width, height, max_n, &probes);
+    if (list.empty()) throw wgtb::NoLegalParameter("the shortlist holds no legal size");
+    std::vector<double> ms(static_cast<std::size_t>(samples));
+    double best = 0.0;
+    wgtb::WorkgroupSize pick = list.front();
+    for (const auto& w : list) {
+      const int rc = sk_stencil_time(desc, d_in, d_out, width, height, pitch, w.cols(), w.rows(), 1, samples, 1,
+                                     ms.data());
+      if (rc != SK_OK) throw wgtb::DeviceError(sk_last_error());
+      std::vector<double> s = ms;
+      std::nth_element(s.begin(), s.begin() + s.size() / 2, s.end());
+      const double med = s[s.size() / 2];
+      if (&w == &list.front() || med < best) {
+        best = med;
+        pick = w;
+      }
+    }
+    *wc = pick.cols();
+    *wr = pick.rows();
+    if (timed) *timed = static_cast<int32_t>(list.size());
+    if (best_ms) *best_ms = best;
+    if (elapsed_ms) {
+      *elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1;
+  }
+}
 
 int wgtb_predict(const char* model_json, const char* kernel_json, const sk_stencil_desc* desc,
                  int64_t width, int64_t height, int32_t* wc, int32_t* wr, int32_t* probes,

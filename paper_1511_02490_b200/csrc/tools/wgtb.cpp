@@ -337,18 +337,24 @@ int cmd_predict(const Args& a) {
   const ProbeFn probe = on_device ? live_probe(s) : ProbeFn([&](WorkgroupSize w) {
     return w.area() <= ctx.effective_max() ? ProbeResult::Legal : ProbeResult::Oversized;
   });
-  WorkgroupSize w;
+  // --shortlist N: the model's N best-ranked accepted sizes, one per line
+  // (the first is the plain prediction)
+  const int n = static_cast<int>(a.num("--shortlist", 0));
+  if (a.has("--shortlist") && n < 1) throw UsageError("--shortlist needs N >= 1");
+  std::vector<WorkgroupSize> ws;
   if (bundle.contains("regressor")) {
     auto model = regressor_from_json(bundle["regressor"]);
     const FitnessMode fm = model->mode() == RegressionMode::Runtime ? FitnessMode::RuntimeReciprocal : FitnessMode::Speedup;
-    w = tune_regress(*model, f, ctx, fm, probe).w;
+    ws = n > 0 ? shortlist_regress(*model, f, ctx, fm, probe, n)
+               : std::vector<WorkgroupSize>{tune_regress(*model, f, ctx, fm, probe).w};
   } else {
     auto model = classifier_from_json(bundle["classifier"]);
     const std::string fb = bundle.value("fallback", "nn");
     FallbackStrategy st = fb == "random" ? FallbackStrategy::random(fnv1a64(s.id, 0)) : FallbackStrategy::nearest_neighbour();
-    w = tune_classify(*model, f, ctx, st, probe).w;
+    ws = n > 0 ? shortlist_classify(*model, f, ctx, st, probe, n)
+               : std::vector<WorkgroupSize>{tune_classify(*model, f, ctx, st, probe).w};
   }
-  std::cout << w.cols() << " " << w.rows() << "\n";
+  for (const auto& w : ws) std::cout << w.cols() << " " << w.rows() << "\n";
   return 0;
 }
 

@@ -68,3 +68,33 @@ def test_refusal_feedback_reproposes_and_never_repeats():
     b2 = torch.empty_like(a2)
     tuned(a2, b2)
     assert tuned.last[2] == 1
+
+
+def test_shortlist_leads_with_the_prediction_and_is_legal():
+    st = Stencil(op="heat", dtype="float32", border="nearest")
+    pred = autotune.predict(st, 4096, 4096, KERNELS / "he.json", MODEL)
+    sl = autotune.shortlist(st, 4096, 4096, KERNELS / "he.json", MODEL, n=8)
+    assert len(sl) == 8 and len(set(sl)) == 8
+    assert sl[0] == (pred["wc"], pred["wr"])
+    for wc, wr in sl:
+        assert wc * wr <= 1024 and wc % 2 == 0 and wr % 2 == 0
+    # a one-size shortlist is the prediction alone
+    assert autotune.shortlist(st, 4096, 4096, KERNELS / "he.json", MODEL, n=1) == sl[:1]
+
+
+def test_tune_measured_picks_the_fastest_of_the_shortlist_and_is_exact():
+    st = Stencil(op="heat", dtype="float32", border="nearest")
+    x = np.random.default_rng(5).random((2048, 2048)).astype(np.float32)
+    a = torch.from_numpy(x).cuda()
+    b = torch.empty_like(a)
+    sl = autotune.shortlist(st, 2048, 2048, KERNELS / "he.json", MODEL, n=6)
+    r = autotune.tune_measured(st, a, b, KERNELS / "he.json", MODEL, n=6, samples=3)
+    assert r["timed"] == len(sl) and (r["wc"], r["wr"]) in sl and r["best_ms"] > 0
+    one = autotune.tune_measured(st, a, b, KERNELS / "he.json", MODEL, n=1, samples=3)
+    assert (one["wc"], one["wr"]) == sl[0] and one["timed"] == 1
+    # the chosen size runs the stencil exactly
+    st(a, b, wc=r["wc"], wr=r["wr"])
+    torch.cuda.synchronize()
+    assert b.cpu().numpy().tobytes() == O.stencil(O.desc_from_stencil(st), x).tobytes()
+    with pytest.raises(RuntimeError):
+        autotune.tune_measured(st, a, b, KERNELS / "he.json", MODEL, n=0)
