@@ -67,9 +67,14 @@ def kernel_label(st, config, W, H, wc, wr):
     """The one-pass kernel a launch at (wc, wr) takes (probe's load path)."""
     lp = st.probe(W, H, wc, wr)["load_path"]
     k = KERNEL_NAMES[config]
+    K = 8  # AUTO's cells per work-item (launch.cu: cells_per_thread)
+    while K > 1 and (wr * K > 64 or wr * K > H):
+        K //= 2
     if lp == "vector":
-        return f"k_stencil_tma<{k}, K, 1024, false, V=4> (16-B vector work-items)"
-    return f"k_stencil_tma<{k}, K, 1024> ({lp})"
+        if K == 8:
+            return f"k_stencil_tma_r80<{k}, K=8, V=4> (16-B vector work-items, 80 registers)"
+        return f"k_stencil_tma<{k}, K={K}, 1024, false, V=4> (16-B vector work-items)"
+    return f"k_stencil_tma<{k}, K={K}, 1024> ({lp})"
 
 
 def measured_hbm_peak():

@@ -349,10 +349,11 @@ __device__ __forceinline__ void store_row_vec(T* __restrict__ out, const Geom& g
   }
 }
 
-template <class Op, typename T, int K, int MAXT, bool PEER = false, int V = 1>
-__global__ void __launch_bounds__(MAXT)
-    k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
-                  const T pad, const __grid_constant__ OpParams<T> p) {
+// The persistent TMA pass, shared by the kernels below (they differ only in
+// their register bound).
+template <class Op, typename T, int K, bool PEER, int V>
+__device__ __forceinline__ void tma_pass(const CUtensorMap& map, T* __restrict__ out, const Geom& g,
+                                         const T pad, const OpParams<T>& p) {
   // Shared memory: [stages x stage_bytes tiles][full[stages]][empty[stages]].
   // full[s]  : 1 arrival (producer's expect_tx) + the TMA transaction bytes.
   // empty[s] : one arrival per warp once it has read the tile in stage s.
@@ -439,9 +440,20 @@ __global__ void __launch_bounds__(MAXT)
       const T* first = tile + (threadIdx.y * K + g.N) * g.tile_w + threadIdx.x * V + g.Wb;
       const int r = r0 + threadIdx.y * K;
       const int c = c0 + threadIdx.x * V;
-      vector_tile<Op, T, K, V>(first, g.tile_w, p, [&](int k, const T (&v)[V]) {
-        store_row_vec<T, K, V>(out, g, r + k, c, edge, v);
-      });
+      if (!edge) {
+        // interior tile: one address per work-item, no bounds test per row
+        T* dst = out + static_cast<long long>(r) * g.pitch_out + c;
+        vector_tile<Op, T, K, V>(first, g.tile_w, p, [&](int k, const T (&v)[V]) {
+          Vec<T, V> x;
+#pragma unroll
+          for (int j = 0; j < V; ++j) x.v[j] = v[j];
+          *reinterpret_cast<Vec<T, V>*>(dst + static_cast<long long>(k) * g.pitch_out) = x;
+        });
+      } else {
+        vector_tile<Op, T, K, V>(first, g.tile_w, p, [&](int k, const T (&v)[V]) {
+          store_row_vec<T, K, V>(out, g, r + k, c, true, v);
+        });
+      }
     } else {
       T res[K];
       compute_tile<Op, T, K>(tile, g, p, res);
@@ -472,6 +484,25 @@ __global__ void __launch_bounds__(MAXT)
       phase ^= 1u;
     }
   }
+}
+
+template <class Op, typename T, int K, int MAXT, bool PEER = false, int V = 1>
+__global__ void __launch_bounds__(MAXT)
+    k_stencil_tma(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
+                  const T pad, const __grid_constant__ OpParams<T> p) {
+  tma_pass<Op, T, K, PEER, V>(map, out, g, pad, p);
+}
+
+// Vector work-items with K = 8 rows: AUTO gives them blocks of wr <= 8 rows
+// and wc <= 63 columns (one TMA box), so at most 504 threads.  1024 threads'
+// 64 registers spill them; 512 threads' bound lets ptxas take 96-115 and
+// costs resident blocks.  80 registers: no spills, and five 128-thread
+// blocks still fit an SM (launchable up to 768 threads).
+template <class Op, typename T, int K, int V>
+__global__ void __maxnreg__(80)
+    k_stencil_tma_r80(const __grid_constant__ CUtensorMap map, T* __restrict__ out, const Geom g,
+                      const T pad, const __grid_constant__ OpParams<T> p) {
+  tma_pass<Op, T, K, false, V>(map, out, g, pad, p);
 }
 
 // --------------------------------------------------------------------- K1b

@@ -23,7 +23,7 @@ KernelPtr vector_for_k(int K) {
     case 1: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 1, MAXT, false, V>);
     case 2: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 2, MAXT, false, V>);
     case 4: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 4, MAXT, false, V>);
-    case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 8, MAXT, false, V>);
+    case 8: return reinterpret_cast<KernelPtr>(&k_stencil_tma_r80<Op, T, 8, V>);
     default: return reinterpret_cast<KernelPtr>(&k_stencil_tma<Op, T, 16, 512, false, V>);  // 128 registers
   }
 }

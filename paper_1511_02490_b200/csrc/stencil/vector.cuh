@@ -197,11 +197,16 @@ __device__ __forceinline__ void vblock_gol(const T* first, int pitch, Emit&& emi
 // Box mean with compile-time extents: per input row the V row sums (west to
 // east), kept for the NR = N + S + 1 rows of the window; cell (k, j) = the
 // row sums of rows k-N .. k+S added north to south, divided by the count.
+// fp32 with count 28: the exact 3-instruction division (div_const_fast) per
+// output row unless a sum of that row is outside its verified range.  (An
+// optimistic form - no branch per row, the work-item re-run on a flag - was
+// measured slower at K = 8: the re-run doubles the kernel's code.)
 template <int N, int S, int E, int W, typename T, int K, int V, class Emit>
 __device__ __forceinline__ void vblock_boxmean(const T* first, int pitch, Emit&& emit) {
   using A = typename Acc<T>::type;
   constexpr int NR = N + S + 1;
   constexpr int kCount = (N + S + 1) * (E + W + 1);
+  constexpr bool kFastDiv = std::is_same_v<T, float> && kCount == 28;
   A rs[NR][V];
   auto row_sums = [&](const T* row, A (&out)[V]) {
     T w[W + V + E];
@@ -240,23 +245,23 @@ __device__ __forceinline__ void vblock_boxmean(const T* first, int pitch, Emit&&
       }
     }
     T out[V];
-    if constexpr (std::is_same_v<T, float> && kCount == 28) {
+    if constexpr (kFastDiv) {
       bool fast = true;
 #pragma unroll
       for (int j = 0; j < V; ++j) fast = fast && div_const_in_range(sum[j]);
-      if (fast && V % 2 == 0) {
+      if (!fast) {  // rare: a sum outside the exact sequence's range
 #pragma unroll
-        for (int j = 0; j + 1 < V; j += 2) {
+        for (int j = 0; j < V; ++j) out[j] = __fdiv_rn(sum[j], static_cast<float>(kCount));
+      } else if constexpr (V % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < V; j += 2) {
           const F2 q = div_const_fast2<kCount>(F2{sum[j], sum[j + 1]});
           out[j] = q.x;
           out[j + 1] = q.y;
         }
-      } else if (fast) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) out[j] = div_const_fast<kCount>(sum[j]);
       } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j) out[j] = __fdiv_rn(sum[j], static_cast<float>(kCount));
+        for (int j = 0; j < V; ++j) out[j] = div_const_fast<kCount>(sum[j]);
       }
     } else {
 #pragma unroll

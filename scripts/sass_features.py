@@ -81,7 +81,7 @@ def main() -> int:
     def counts_for(op: str) -> dict[str, int]:
         # the kernel AUTO runs for fp32: the vector work-item instantiation
         # when the op has one (vector.cuh), else the scalar one-pass kernel
-        vec = re.compile(rf"void sk::k_stencil_tma<sk::{re.escape(op)}, float, 8, 1024, false, 4>\(")
+        vec = re.compile(rf"void sk::k_stencil_tma_r80<sk::{re.escape(op)}, float, 8, 4>\(")
         hits = [n for n in funcs if vec.match(n)]
         if hits:
             return categorise(funcs[hits[0]])

@@ -393,12 +393,15 @@ def test_streamed_host_jobs_match_run_host():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("path", ["auto", "explicit"])
-def test_boxmean_division_special_values(path):
+@pytest.mark.parametrize("path,wc,wr", [("auto", 64, 4), ("explicit", 64, 4), ("vector", 16, 8),
+                                        ("vector", 8, 2), ("vector", 32, 4)])
+def test_boxmean_division_special_values(path, wc, wr):
     """Config-4 boxmean divides by 28 with the exact 3-instruction sequence
     (ops.cuh div_const_fast) and falls back to IEEE division for a
     work-item whose sums include zeros, subnormals, huge values or inf:
-    both branches must equal the oracle's s / 28 bit for bit."""
+    both branches must equal the oracle's s / 28 bit for bit.  The vector
+    kernel divides optimistically and re-runs such a work-item with the fp64
+    form (vector.cuh vblock_boxmean_exact)."""
     import torch
 
     rng = np.random.default_rng(12)
@@ -412,7 +415,7 @@ def test_boxmean_division_special_values(path):
                  border="nearest", load_path=path)
     a = torch.from_numpy(x).cuda()
     b = torch.empty_like(a)
-    st(a, b, 64, 4)
+    st(a, b, wc, wr)
     torch.cuda.synchronize()
     want = O.stencil(O.desc_from_stencil(st), x)
     assert b.cpu().numpy().tobytes() == want.tobytes()
