@@ -76,6 +76,13 @@ def test_bad_fields_rejected(field, value):
 
 
 def test_wgtb_c_api_exports():
+    """libwgtb exports every function include/wgtb_c.h declares."""
+    import re
+
     from paper_1511_02490_b200 import autotune
     lib = autotune.lib()
-    assert hasattr(lib, "wgtb_predict") and hasattr(lib, "wgtb_last_error")
+    header = (N.REPO_ROOT / "include" / "wgtb_c.h").read_text()
+    names = set(re.findall(r"^(?:int|void|const char\*)\s+(wgtb_\w+)\(", header, re.M))
+    assert {"wgtb_predict", "wgtb_shortlist", "wgtb_tune_measured", "wgtb_launch_tuned"} <= names
+    for n in names:
+        assert hasattr(lib, n), n
