@@ -9,6 +9,7 @@
 //                  block can be resident, or the launch reports a
 //                  (non-sticky) configuration/resource error.
 #include <cstdarg>
+#include <numeric>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -48,6 +49,32 @@ bool pdl_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// Persistent grid size.  CTA b visits tiles b, b + G, b + 2G, ... of the
+// row-major tile list, so its tile columns stay in one residue class modulo
+// d = gcd(G, tiles_x).  G = occupancy x 148 SMs is a multiple of 148 = 4 x 37:
+// at tiles_x = 74 or 37 (heat 16384^2 at 56 x wr or 224 x 4) every tile of
+// the CTAs in column 0 and column tiles_x-1 is an edge tile (border fix-up,
+// two block barriers, bounds-checked stores) and the launch waits for them:
+// 1.7-2.1x the neighbouring sizes in the sweep.  Dropping a few CTAs from the
+// grid to reach d <= 2 spreads the edge columns over every CTA's cycle; the
+// cost is at most 1/G of the resident slots.  SK_GRID_BALANCE=0 disables it.
+int balanced_grid(int grid, int tiles_x) {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_GRID_BALANCE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || tiles_x <= 2) return grid;
+  int best = grid, best_d = std::gcd(grid, tiles_x);
+  for (int G = grid - 1; best_d > 2 && G >= std::max(1, grid - 32); --G) {
+    const int dd = std::gcd(G, tiles_x);
+    if (dd < best_d) {
+      best = G;
+      best_d = dd;
+    }
+  }
+  return best;
 }
 
 cudaError_t launch_tma(const void* kernel, dim3 grid, dim3 block, void** args, int smem, cudaStream_t stream) {
@@ -603,6 +630,7 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
   long long ntiles = static_cast<long long>(g.tiles_x) * g.tiles_y;
   plan->grid = static_cast<int>(std::min<long long>(ntiles, static_cast<long long>(occ) * info.sms));
+  if (plan->grid < ntiles) plan->grid = balanced_grid(plan->grid, g.tiles_x);
   return SK_OK;
 }
 

@@ -474,3 +474,21 @@ def test_iterate_graph_replay_matches_oracle(op, dtype, tb, iters):
         got = st.iterate(a, b, iters, 16, 4)
         torch.cuda.synchronize()
         assert got.cpu().numpy().tobytes() == want.tobytes(), f"call {call}"
+
+
+@pytest.mark.parametrize("op,dtype,W,wc,wr,border", [
+    ("heat", "float32", 16384, 56, 4, "nearest"),   # vector, tiles_x = 74 (divides the 148-SM grid)
+    ("heat", "float32", 16384, 224, 4, "nearest"),  # scalar TMA, tiles_x = 74
+    ("heat", "int32", 8192, 28, 8, "nearest"),      # vector, tiles_x = 74
+    ("boxmean", "float32", 4096, 28, 8, "nearest"),  # vector, tiles_x = 37
+    ("gol", "int32", 8192, 112, 2, "pad"),           # scalar TMA, tiles_x = 74, pad 0
+])
+def test_balanced_grid_matches_oracle(op, dtype, W, wc, wr, border):
+    """Sizes whose tile-column count divides 148 x occupancy: the persistent
+    grid is trimmed so edge columns rotate over every CTA (launch.cu
+    balanced_grid).  Tall enough that each CTA runs several tiles."""
+    kw = dict(north=5, south=1, east=3, west=0) if op == "boxmean" else {}
+    st = Stencil(op=op, dtype=dtype, border=border, **kw)
+    x = rand_grid(dtype, (96, W), 31, op)
+    want = O.stencil(O.desc_from_stencil(st), x)
+    assert_same(gpu_pass(st, x, wc, wr), want, f"{op} {W} at {wc}x{wr}")
