@@ -404,6 +404,19 @@ EncodeTiledFn encode_fn() {
 
 std::map<MapKey, CUtensorMap> g_maps;
 
+// L2 fill granularity of the tile loads (SK_L2_PROMO=0/64/128/256 for A/B).
+CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char* e = std::getenv("SK_L2_PROMO");
+    const int v = e ? std::atoi(e) : 256;
+    return v == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+           : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                      : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return p;
+}
+
 int tensor_map(const MapKey& key, CUtensorMap* out) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -424,8 +437,8 @@ int tensor_map(const MapKey& key, CUtensorMap* out) {
   cuuint32_t estr[2] = {1, 1};
   CUtensorMap m;
   CUresult r = fn(&m, dt, 2, const_cast<void*>(key.base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_maps.size() > 4096) g_maps.clear();
