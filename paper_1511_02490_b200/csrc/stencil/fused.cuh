@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(MAXT)
   const int nthreads = blockDim.x * blockDim.y;
   const int nwarps = (nthreads + 31) >> 5;
   const int ntiles = g.tiles_x * g.tiles_y;
-  const int lag = g.stages >= 3 ? 2 : 1;
+  const int lag = g.lag > 0 ? g.lag : g.stages >= 3 ? 2 : 1;
   const int lane = tid & 31;
   const int warp_lanes = min(32, nthreads - (tid & ~31));
   const unsigned warp_mask = warp_lanes == 32 ? 0xffffffffu : ((1u << warp_lanes) - 1u);

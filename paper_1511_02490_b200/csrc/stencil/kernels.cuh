@@ -79,6 +79,7 @@ struct Geom {
   int sp;                   // row pitch of the two scratch generation buffers
   int scratch_elems;        // elements per scratch buffer (incl. K slack rows)
   PeerTile peer;            // fused peer exchange (PEER kernels only)
+  int lag;                  // ring refill lag (0: 2 for >= 3 stages, else 1)
 };
 
 // ------------------------------------------------------------------ PTX glue
@@ -367,7 +368,7 @@ __device__ __forceinline__ void tma_pass(const CUtensorMap& map, T* __restrict__
   const bool fix_edges = !(g.mode == 0 && g.pad_is_zero);
   // Refill lag: the stage read `lag` iterations ago is refilled, so the
   // producer rarely waits for slow warps (lag 1 for shallow rings).
-  const int lag = g.stages >= 3 ? 2 : 1;
+  const int lag = g.lag > 0 ? g.lag : g.stages >= 3 ? 2 : 1;
   const int lane = tid & 31;
   const int warp_lanes = min(32, nthreads - (tid & ~31));
   const unsigned warp_mask = warp_lanes == 32 ? 0xffffffffu : ((1u << warp_lanes) - 1u);

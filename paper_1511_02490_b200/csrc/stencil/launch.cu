@@ -637,7 +637,34 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   long long share = (static_cast<long long>(info.smem_per_sm) / blocks) - 1024 - 128 - scratch;
   int stages = static_cast<int>(std::clamp<long long>(share / stage, 1, 8));
   while (stages > 1 && stage * stages + scratch + 128 > attr.max_dyn_smem) --stages;
+  // A/B knobs (unset: the policy above): SK_MIN_STAGES deepens the ring at the
+  // cost of resident blocks; SK_RING_LAG sets the refill lag (prefetch depth
+  // = stages - lag tiles).
+  static const int min_stages = [] {
+    const char* e = std::getenv("SK_MIN_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int ring_lag = [] {
+    const char* e = std::getenv("SK_RING_LAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (min_stages > stages && stage * min_stages + scratch + 128 <= attr.max_dyn_smem) stages = min_stages;
+  // A two-stage ring has no slack: the refill of tile i+1 waits for the
+  // slowest warp of tile i-1.  When the share policy leaves at most two
+  // resident blocks with two stages each, one block with a three-stage ring
+  // (lag 2: one tile ahead plus one stage of slack) is faster: heat 16384^2
+  // vector 48x8 389 -> 360 us, 40x8 397 -> 356 (profiles/r04_ring_probe.jsonl).
+  // Blocks of many small tiles (box mean 16x8: five blocks) keep the policy.
+  static const bool deep_ring = [] {
+    const char* e = std::getenv("SK_DEEP_RING");
+    return !(e && e[0] == '0');
+  }();
+  if (deep_ring && min_stages == 0 && TB == 1 && stages < 3 && blocks <= 2 &&
+      stage * 3 + scratch + 128 <= attr.max_dyn_smem) {
+    stages = 3;
+  }
   g.stages = stages;
+  g.lag = ring_lag > 0 ? std::min(ring_lag, std::max(1, stages - 1)) : 0;
   plan->smem = static_cast<int>(stage * stages + scratch + 16 * stages);  // + full/empty barriers
   int occ = occupancy(dev, plan->kernel, plan->threads, plan->smem, drv);
   if (occ < 1) return fail(SK_REFUSED, "no resident block possible for %dx%d", wc, wr);
