@@ -653,13 +653,16 @@ int make_plan(const sk_stencil_desc& d, long long W, long long H, long long pitc
   // slowest warp of tile i-1.  When the share policy leaves at most two
   // resident blocks with two stages each, one block with a three-stage ring
   // (lag 2: one tile ahead plus one stage of slack) is faster: heat 16384^2
-  // vector 48x8 389 -> 360 us, 40x8 397 -> 356 (profiles/r04_ring_probe.jsonl).
-  // Blocks of many small tiles (box mean 16x8: five blocks) keep the policy.
+  // vector 48x8 393 -> 357 us, 40x8 400 -> 352 (profiles/r04_landscape_ab.jsonl).
+  // Only the light 3x3 / cross ops: the box mean's 28 instructions per cell
+  // need the second block's warps (36x8 27.7 -> 34.9 us with one block;
+  // landscape A/B in profiles/r04_landscape_ab.jsonl).
   static const bool deep_ring = [] {
     const char* e = std::getenv("SK_DEEP_RING");
     return !(e && e[0] == '0');
   }();
-  if (deep_ring && min_stages == 0 && TB == 1 && stages < 3 && blocks <= 2 &&
+  const bool light_op = d.op == SK_OP_HEAT || d.op == SK_OP_FIVE_POINT || d.op == SK_OP_GOL;
+  if (deep_ring && light_op && min_stages == 0 && TB == 1 && stages < 3 && blocks <= 2 &&
       stage * 3 + scratch + 128 <= attr.max_dyn_smem) {
     stages = 3;
   }
