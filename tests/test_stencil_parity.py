@@ -492,3 +492,18 @@ def test_balanced_grid_matches_oracle(op, dtype, W, wc, wr, border):
     x = rand_grid(dtype, (96, W), 31, op)
     want = O.stencil(O.desc_from_stencil(st), x)
     assert_same(gpu_pass(st, x, wc, wr), want, f"{op} {W} at {wc}x{wr}")
+
+
+@pytest.mark.parametrize("op,dtype,wc,wr,border", [
+    ("heat", "float32", 48, 8, "nearest"),       # 2 blocks x 2 stages -> 1 block x 3 stages
+    ("heat", "float32", 40, 8, "nearest"),
+    ("five_point", "float32", 44, 8, "pad"),
+    ("gol", "int32", 48, 8, "pad"),
+])
+def test_deep_ring_matches_oracle(op, dtype, wc, wr, border):
+    """Launches the ring-depth rule reshapes (launch.cu make_plan: one block
+    with a three-stage ring, lag 2): several tiles per CTA so the ring wraps."""
+    st = Stencil(op=op, dtype=dtype, border=border)
+    x = rand_grid(dtype, (520, 8192), 41, op)
+    want = O.stencil(O.desc_from_stencil(st), x)
+    assert_same(gpu_pass(st, x, wc, wr), want, f"{op} at {wc}x{wr}")
