@@ -136,9 +136,13 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
   char* src = static_cast<char*>(d_a);
   char* dst = static_cast<char*>(d_b);
   auto row = [&](char* base, long long r) { return base + (N + r) * rb; };  // owned row r
+  const int swc = es == 8 ? 124 : 62;
+  const bool strips = N > 0 || S > 0;
   for (int it = 0; it < iterations; ++it) {
+    // generation start: src is complete on the caller's stream
+    if (cudaEventRecord(cs->ready, st) != cudaSuccess) return fail(SK_ECUDA, "generation ordering failed");
     if (nranks > 1) {
-      if (cudaEventRecord(cs->ready, st) != cudaSuccess || cudaStreamWaitEvent(cs->stream, cs->ready, 0) != cudaSuccess) {
+      if (cudaStreamWaitEvent(cs->stream, cs->ready, 0) != cudaSuccess) {
         return fail(SK_ECUDA, "exchange ordering failed");
       }
       if (int rc = nccl_check(n.group_start(), "ncclGroupStart")) return rc;
@@ -156,41 +160,29 @@ extern "C" int sk_stencil_iterate_nccl(const sk_stencil_desc* desc, void* d_a, v
       if (rc_end != SK_OK) return rc_end;
       if (cudaEventRecord(cs->halo, cs->stream) != cudaSuccess) return fail(SK_ECUDA, "exchange event failed");
     }
-    // interior: reads owned rows only, runs while the halos are in flight
-    const long long inner = rows - N - S;
-    if (inner > 0) {
-      if (int rc = launch(one, row(src, N), row(dst, N), width, inner, pitch, pitch, N, S, wc, wr, st)) return rc;
-    }
-    if (nranks > 1 && cudaStreamWaitEvent(st, cs->halo, 0) != cudaSuccess) {
-      return fail(SK_ECUDA, "exchange wait failed");
-    }
-    // the two strips are independent, a few dozen blocks each: the south one
-    // runs on a side stream beside the north one (their latencies overlap)
-    const bool two = N > 0 && S > 0;
-    if (two && (cudaEventRecord(cs->south, st) != cudaSuccess ||
-                cudaStreamWaitEvent(cs->side, cs->south, 0) != cudaSuccess)) {
+    // Boundary strips on the side stream, behind the halo (or the generation
+    // start at one rank), queued before the interior so their few CTAs are
+    // resident beside the persistent interior grid instead of after it.
+    if (strips && cudaStreamWaitEvent(cs->side, nranks > 1 ? cs->halo : cs->ready, 0) != cudaSuccess) {
       return fail(SK_ECUDA, "strip ordering failed");
     }
-    // boundary strips: their halo rows are real data inside the grid, border
-    // cells at the global edges (rows_above / rows_below = 0 there).  A
-    // strip is a few rows tall, so it runs one-row workgroups 248 cells wide
-    // (62 vector work-items of 4 cells, or 124 of 2 for fp64): the tuned
-    // wc x wr tile would be mostly rows beyond the strip - edge tiles with a
-    // fix-up pass each - for one or two useful rows.
-    const int swc = es == 8 ? 124 : 62;
     if (N > 0) {
-      if (int rc = launch(one, row(src, 0), row(dst, 0), width, N, pitch, pitch, has_n ? N : 0, S, swc, 1, st)) {
+      if (int rc = launch(one, row(src, 0), row(dst, 0), width, N, pitch, pitch, has_n ? N : 0, S, swc, 1, cs->side)) {
         return rc;
       }
     }
     if (S > 0) {
       if (int rc = launch(one, row(src, rows - S), row(dst, rows - S), width, S, pitch, pitch, N, has_s ? S : 0,
-                          swc, 1, two ? cs->side : st)) {
+                          swc, 1, cs->side)) {
         return rc;
       }
     }
-    if (two && (cudaEventRecord(cs->south, cs->side) != cudaSuccess ||
-                cudaStreamWaitEvent(st, cs->south, 0) != cudaSuccess)) {
+    const long long inner = rows - N - S;
+    if (inner > 0) {
+      if (int rc = launch(one, row(src, N), row(dst, N), width, inner, pitch, pitch, N, S, wc, wr, st)) return rc;
+    }
+    if (strips && (cudaEventRecord(cs->south, cs->side) != cudaSuccess ||
+                   cudaStreamWaitEvent(st, cs->south, 0) != cudaSuccess)) {
       return fail(SK_ECUDA, "strip join failed");
     }
     std::swap(src, dst);
