@@ -177,8 +177,9 @@ int sk_stencil_iterate(const sk_stencil_desc* desc, void* d_a, void* d_b, int64_
  * Per generation: ncclGroupStart; send the first S owned rows to rank-1 and
  * receive N halo rows from it; send the last N owned rows to rank+1 and
  * receive S halo rows from it; ncclGroupEnd - on an internal exchange
- * stream, while the interior rows [N, rows-S) compute on `stream`; then the
- * two boundary strips.  Rank 0's north and rank nranks-1's south halos are
+ * stream; the two boundary strips on an internal side stream behind the
+ * exchange, beside the interior rows [N, rows-S) on `stream`, which then
+ * joins the side stream.  Rank 0's north and rank nranks-1's south halos are
  * border cells (pad / nearest), so the ranks together compute exactly the
  * single-GPU result.  `comm` is an ncclComm_t of the NCCL loaded in the
  * process (resolved at run time; the library does not link NCCL), with
